@@ -1,0 +1,433 @@
+"""Benchmark: circuit evaluations/s, forward+backward, log semiring.
+
+Workload (BASELINE.json configs[2]): the 1,016,536-node
+d-DNNF compiled from gen_3cnf(56, 128, seed 1) (data/circuits/C.npz), log
+semiring fp32, 1024 batch rows per GPU (weak scaling), Philox(key=0) weights
+p ~ U(0.05, 0.95) per literal. One step = forward (trace retained) +
+backward (all-ones seed) over one batch; with N > 1 ranks each rank owns its
+own 1024 rows and the root outputs are all-gathered over NCCL.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line. `value` = device-timed evals/s with inputs
+resident in HBM (CUDA events, max over ranks); `e2e` = the same metric
+through the public API (engine.forward_log + engine.backward with host numpy
+arrays; H2D of the weights and D2H of roots + grads inside the timed region);
+`roofline` = the dominant kernel's algorithmic bytes / its event-timed
+duration (per-launch CUDA events in a separate instrumented step);
+`cpu_baseline` = the CPU oracle (numpy restatement of the reference engine)
+on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "circuit evals/sec (fwd+bwd, log semiring) vs nodes; HBM roofline fraction"
+CIRCUIT = os.path.join(ROOT, "data", "circuits", "C.npz")
+WORKLOAD = "C: gen_3cnf(56,128,seed=1) -> compile_cnf -> layerize -> tensorize (1,016,536 nodes)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------
+
+def layer_bytes(tc, s, B, domain="log"):
+    """Per-launch algorithmic bytes of every forward and backward layer kernel.
+    fwd_l = s*B*(W_{l-1}+W_l) + 4*(E_l+W_l+1);
+    bwd_l = c_l*s*B*(W_{l-1}+W_l) + 4*(2E_l+W_{l-1}+1), c_l = 2 for log-sum
+    (and real-product) layers, 1 for pass-through layers."""
+    fwd, bwd = {}, {}
+    prev = tc.num_inputs
+    for l, layer in enumerate(tc.layers, start=1):
+        W, E = layer.width, len(layer.sources)
+        heavy = (layer.op != "prod") if domain == "log" else (layer.op == "prod")
+        c = 2 if heavy else 1
+        fwd[l] = s * B * (prev + W) + 4 * (E + W + 1)
+        bwd[l] = c * s * B * (prev + W) + 4 * (2 * E + prev + 1)
+        prev = W
+    return fwd, bwd
+
+
+def bytes_per_eval(tc, s, B):
+    fwd, bwd = layer_bytes(tc, s, B)
+    return (sum(fwd.values()) + sum(bwd.values())) / B
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+
+_W_TC = None
+
+
+def _worker_init(path):
+    global _W_TC
+    from paper_2410_11415_b200.tensorized import load_npz
+    from oracle import engine_port as oracle
+    _W_TC = load_npz(path)
+    oracle.plans(_W_TC)
+
+
+def _worker_run(args):
+    """One bounded chunk: fwd (fp32, log, trace) + bwd on `rows` rows."""
+    from oracle import engine_port as oracle
+    seed, rows = args
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    w = np.log(rng.uniform(0.05, 0.95, size=(rows, _W_TC.num_inputs))).astype(np.float32)
+    t0 = time.perf_counter()
+    _, tr = oracle.forward(_W_TC, w, "log")
+    oracle.backward(_W_TC, tr, "log")
+    return rows, time.perf_counter() - t0
+
+
+def cpu_pool_size(per_worker_gb=1.0):
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available / 2 ** 30
+        n = max(1, min(n, int(avail * 0.6 / per_worker_gb)))
+    except Exception:
+        pass
+    return max(1, min(n, 64))
+
+
+class CpuOracle:
+    """A fork pool of oracle workers, each evaluating independent row chunks
+    (the reference engine is single-threaded numpy; rows are independent,
+    so P processes is the best CPU arrangement)."""
+
+    def __init__(self, path, rows_per_task=16):
+        import multiprocessing as mp
+        self.procs = cpu_pool_size()
+        self.rows = rows_per_task
+        ctx = mp.get_context("fork")
+        self.pool = ctx.Pool(self.procs, initializer=_worker_init, initargs=(path,))
+        self.pool.map(_worker_run, [(i, 1) for i in range(self.procs)])  # warm plans
+
+    def step(self, tasks_per_proc=1, seed0=0):
+        tasks = [(seed0 + i, self.rows) for i in range(self.procs * tasks_per_proc)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_worker_run, tasks, chunksize=1)
+        wall = time.perf_counter() - t0
+        return sum(r for r, _ in res), wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0  # rank 0 alone runs the CPU reference
+    from paper_2410_11415_b200.tensorized import load_npz
+    tc = load_npz(CIRCUIT)
+    cpu = CpuOracle(CIRCUIT)
+    for i in range(args.warmup):
+        cpu.step(seed0=1000 * i)
+    rows = 0
+    wall = 0.0
+    for i in range(args.steps):
+        r, t = cpu.step(seed0=10_000 + 1000 * i)
+        rows += r
+        wall += t
+    cpu.close()
+    value = rows / wall
+    nodes = tc.num_inputs + sum(l.width for l in tc.layers)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "nodes": nodes,
+                   "edges": int(sum(len(l.sources) for l in tc.layers)),
+                   "semiring": "log", "pass": "fwd+bwd",
+                   "rows_per_step": cpu.procs * cpu.rows},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cpu.procs, "kind": "port",
+                         "sample": f"{cpu.procs} processes x {cpu.rows} rows per step, "
+                                   "oracle/engine_port.py (numpy restatement of "
+                                   "laycirc/engine.py), fp32 log fwd+bwd"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    from paper_2410_11415_b200 import engine, _lib
+    from paper_2410_11415_b200.tensorized import load_npz
+
+    tc = load_npz(CIRCUIT)
+    B = args.batch
+    s = 4  # fp32
+    dt = np.float32
+
+    # CPU baseline first (rank 0, N = 1 only), before CUDA is initialised,
+    # so the fork pool never inherits a CUDA context.
+    cpu_line = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = CpuOracle(CIRCUIT)
+        cpu.step(seed0=77)
+        rows = wall = 0
+        t_end = time.perf_counter() + args.cpu_seconds
+        i = 0
+        while time.perf_counter() < t_end or i == 0:
+            r, t = cpu.step(seed0=100 + 1000 * i)
+            rows += r
+            wall += t
+            i += 1
+        cpu.close()
+        cpu_line = {"value": rows / wall, "unit": "evals/s", "cores": cpu.procs, "kind": "port",
+                    "sample": f"{rows} rows of config C in {wall:.1f} s ({cpu.procs} processes x "
+                              f"{cpu.rows}-row chunks), oracle/engine_port.py, fp32 log fwd+bwd"}
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    plan = engine.device_plan(tc, dev)
+
+    rng = np.random.Generator(np.random.Philox(key=0))
+    w_all = np.log(rng.uniform(0.05, 0.95, size=(B * world, tc.num_inputs)))
+    w_host = w_all[rank * B:(rank + 1) * B]
+    w_dev = torch.from_numpy(w_host.astype(np.float32)).to(dev)
+    values = plan.alloc_values(B, dt, retain=True)
+    outputs = torch.empty((B, tc.num_roots), dtype=torch.float32, device=dev)
+    grads = torch.empty((B, tc.num_inputs), dtype=torch.float32, device=dev)
+    work = plan.workspace(B, dt)
+    gathered = [torch.empty_like(outputs) for _ in range(world)] if world > 1 else None
+
+    def step():
+        plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
+        plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
+        if world > 1:
+            dist.all_gather(gathered, outputs)
+
+    stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    n0 = lib.klay_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = lib.klay_launch_count() - n0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    clk = clocks.stop()
+    ms_per_step = ms / args.steps
+    value = world * B / (ms_per_step / 1e3)
+
+    # ---- per-launch timing of one instrumented step (roofline) ----------
+    lib.klay_profiler_begin()
+    plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
+    plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
+    import ctypes
+    cap = 4 * len(tc.layers) + 16
+    kinds = (ctypes.c_int32 * cap)()
+    layers = (ctypes.c_int32 * cap)()
+    tms = (ctypes.c_float * cap)()
+    nrec = ctypes.c_int32()
+    lib.klay_profiler_end(cap, kinds, layers, tms, ctypes.byref(nrec))
+    fwd_b, bwd_b = layer_bytes(tc, s, B)
+    per_kind = {0: [0.0, 0.0, 0], 1: [0.0, 0.0, 0]}
+    other_ms = 0.0
+    for i in range(min(nrec.value, cap)):
+        k, l, t = kinds[i], layers[i], tms[i]
+        if k in (0, 1):
+            per_kind[k][0] += t
+            per_kind[k][1] += (fwd_b if k == 0 else bwd_b)[l]
+            per_kind[k][2] += 1
+        else:
+            other_ms += t
+    peak, peak_kind = load_peaks()
+    dom = max(per_kind, key=lambda k: per_kind[k][0])
+    dms, dbytes, dn = per_kind[dom]
+    achieved = dbytes / (dms / 1e3) / 1e9
+    bpe = bytes_per_eval(tc, s, B)
+
+    # ---- e2e: public API with host buffers ------------------------------
+    e2e = None
+    if not args.no_e2e:
+        W = engine.WeightAssignment(w_host, "log")
+        for _ in range(2):
+            tr = engine.forward_log(tc, W, dtype=np.float32)
+            engine.backward(tc, tr)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(3, min(args.steps, 10))
+        for _ in range(n_e2e):
+            tr = engine.forward_log(tc, W, dtype=np.float32)
+            g = engine.backward(tc, tr)
+        torch.cuda.synchronize(dev)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * B * n_e2e / el, "unit": "evals/s",
+               "h2d_bytes_per_step": int(w_host.nbytes),
+               "d2h_bytes_per_step": int(tr.outputs.nbytes + g.nbytes),
+               "api": "engine.forward_log(dtype=float32) + engine.backward, numpy in/out"}
+
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    nodes = tc.num_inputs + sum(l.width for l in tc.layers)
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "nodes": nodes,
+                   "edges": int(sum(len(l.sources) for l in tc.layers)),
+                   "gate_layers": len(tc.layers), "semiring": "log", "pass": "fwd+bwd",
+                   "batch_per_gpu": B, "global_batch": B * world,
+                   "parallelism": f"dp{world} (batch-sharded, plan replicated)",
+                   "l2": f"no flush: per-step working set {nodes * B * s / 1e9:.2f} GB trace "
+                         ">> 126 MB L2",
+                   "bytes_per_eval": bpe,
+                   "step_roofline_frac": value / world * bpe / (peak * 1e9)},
+        "roofline": {"bound": "hbm", "kernel": ["fwd_layer_kernel", "bwd_layer_kernel"][dom],
+                     "launches_per_step": dn, "achieved": achieved, "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "kernel_ms_per_step": dms,
+                     "fwd_ms": per_kind[0][0], "bwd_ms": per_kind[1][0],
+                     "boundary_ms": other_ms},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "cpu_baseline": cpu_line,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1024, help="rows per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

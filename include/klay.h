@@ -1,0 +1,139 @@
+/*
+ * libklay — B200 (sm_100a) evaluator for layered arithmetic circuits.
+ *
+ * Plain C ABI: host pointers / device pointers / sizes only, no torch types.
+ * Every entry point replaces one function of the reference evaluation engine
+ * (/root/reference/pkg/src/laycirc/engine.py); the mapping is cited per call.
+ * The reference is pure Python + numpy, so it has no FFI of its own; the
+ * binding a maintainer would add is the ctypes stub in INTEGRATION.md, which
+ * is exactly what paper_2410_11415_b200/_lib.py does.
+ *
+ * Value layout ("node-major"): one contiguous device buffer of rows, one row
+ * per circuit node, `ld` elements per row (ld >= B, ld*sizeof(T) a multiple
+ * of 16 bytes). Row order: the K input slots, then layer 1 .. layer L nodes
+ * in the reference's within-layer order (indices are never permuted).
+ *
+ * Return codes: 0 = ok, otherwise a KLAY_E* code; klay_last_error() gives a
+ * thread-local message. All device work is stream-ordered on `stream`
+ * (a cudaStream_t; NULL = legacy default stream). No call allocates device
+ * memory except klay_plan_create.
+ */
+#ifndef KLAY_H
+#define KLAY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KLAY_OK 0
+#define KLAY_EINVAL 1       /* bad argument / shape (maps to EvalError)       */
+#define KLAY_EFORMAT 2      /* circuit invariant violated (KlayFormatError)   */
+#define KLAY_ECUDA 3        /* CUDA runtime / launch failure                  */
+#define KLAY_EUNSUPPORTED 4 /* semiring/domain combination not defined        */
+
+/* semirings (engine.py:158-193, forward_log 247-282) */
+#define KLAY_REAL 0
+#define KLAY_LOG 1
+#define KLAY_BOOL 2
+#define KLAY_MAXPROD 3
+
+/* element types */
+#define KLAY_F32 0
+#define KLAY_F64 1
+
+typedef struct KlayPlan KlayPlan;
+
+/* Library version string. */
+const char* klay_version(void);
+
+/* Thread-local message for the last nonzero return code of this thread. */
+const char* klay_last_error(void);
+
+/*
+ * Build the immutable device plan of a tensorized circuit and upload it to
+ * `device`. Replaces engine._plans (engine.py:138-155): per layer the CSR
+ * offsets of the parent segments and the stable, ascending-edge-order
+ * transposed CSR (child -> parents) used by the atomic-free backward.
+ *
+ *   widths[L], edge_counts[L]        per gate layer (TensorLayer.width / num_edges)
+ *   sources, segments                concatenation over layers of
+ *                                    TensorLayer.sources / .segments (int64,
+ *                                    tensorize.py:47-48)
+ *   root_nodes[R]                    final-layer index per root position, or -1
+ *                                    for a constant root (root_indices +
+ *                                    constant_roots, tensorize.py:65-76)
+ *   const_vals[R]                    1/0 value of constant roots (ignored else)
+ * The structural invariants of tensorize.py:94-132 are re-checked on the
+ * host; a violation returns KLAY_EFORMAT.
+ */
+int klay_plan_create(int64_t num_inputs, int32_t num_layers, const int64_t* widths,
+                     const int64_t* edge_counts, const int64_t* sources,
+                     const int64_t* segments, int32_t num_roots, const int64_t* root_nodes,
+                     const int8_t* const_vals, int32_t device, KlayPlan** out);
+
+int klay_plan_destroy(KlayPlan* plan);
+
+/* Sum of all layer widths including the K input rows (= trace rows). */
+int64_t klay_plan_num_nodes(const KlayPlan* plan);
+/* Largest row count of any single layer (inputs included). */
+int64_t klay_plan_max_width(const KlayPlan* plan);
+/* Row offset of layer l (0 = inputs) inside the trace buffer. */
+int64_t klay_plan_layer_offset(const KlayPlan* plan, int32_t layer);
+
+/* Smallest legal row stride (elements) for batch B and element type. */
+int64_t klay_row_stride(int64_t batch, int32_t dtype);
+
+/*
+ * Forward pass. Replaces forward_real / forward_log / evaluate_semiring
+ * (engine.py:226-304) including _run_layers (215-223) and _assemble_outputs
+ * (203-212).
+ *   weights      device [B, K] row-major, element type `weights_dtype`
+ *                (values in the semiring's domain: log values for KLAY_LOG)
+ *   values       retain != 0: trace buffer [num_nodes, ld] (every layer kept,
+ *                EvalTrace.node_values); retain == 0: scratch of
+ *                2 * max_width rows (ping-pong, only the last layer survives)
+ *   outputs      device [B, R] row-major, element type `dtype` (may be NULL)
+ *   epsilon      log semiring only, added inside the log (must be >= 0)
+ */
+int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
+                 const void* weights, int32_t weights_dtype, void* values, int64_t ld,
+                 int32_t retain, void* outputs, int64_t batch, double epsilon,
+                 void* stream);
+
+/*
+ * Backward pass over a retained trace. Replaces engine.backward
+ * (engine.py:307-355) with _product_adjoint (358-369): gradient of
+ * sum_r seed[:, r] * root_r w.r.t. the K input slots.
+ *   domain       KLAY_REAL or KLAY_LOG (the trace's domain)
+ *   seed         device [B, R] row-major in `dtype`, or NULL for all-ones
+ *   grads        device [B, K] row-major in `dtype`
+ *   workspace    device scratch of klay_backward_workspace() bytes
+ */
+int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
+                  int64_t ld, const void* seed, void* grads, void* workspace,
+                  int64_t batch, void* stream);
+
+size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
+
+/* ---- instrumentation (no counterpart in the reference) ---------------- */
+
+/* Number of kernels this library has launched so far (process-wide). */
+int64_t klay_launch_count(void);
+
+/* Time every subsequent launch of this thread with CUDA events on its
+ * stream until klay_profiler_end (which synchronizes). Record kinds:
+ * 0 = forward layer kernel, 1 = backward layer kernel, 2 = forward
+ * boundary (inputs / outputs), 3 = backward boundary (seeds / grads);
+ * `layers` holds the 1-based gate layer (0 / L+1 for boundary kernels). */
+int klay_profiler_begin(void);
+int klay_profiler_end(int32_t max_records, int32_t* kinds, int32_t* layers, float* ms,
+                      int32_t* n_records);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KLAY_H */

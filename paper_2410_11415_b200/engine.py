@@ -1,0 +1,470 @@
+"""Batched forward/backward evaluation of tensorized circuits on B200.
+
+Drop-in mirror of the reference engine API
+(``/root/reference/pkg/src/laycirc/engine.py``): ``WeightAssignment``,
+``weights_from_*``, ``EvalTrace``, ``Semiring`` / ``REAL`` / ``BOOLEAN`` /
+``MAX_PRODUCT``, ``forward_real``, ``forward_log``, ``evaluate_semiring``,
+``backward``, ``gradient`` — same names, argument meaning, return shapes and
+``EvalError`` behaviour. Any object with the reference ``TensorizedCircuit``
+attributes is accepted (including a reference instance).
+
+Every layer runs in ``libklay.so`` (hand-written sm_100a kernels, C ABI in
+``include/klay.h``); there is no CPU fallback. Host numpy arrays in and out,
+as in the reference; ``DevicePlan`` is the device-resident fast path used by
+the torch module and the benchmark (inputs already in HBM).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from . import _lib
+from .tensorized import PRODUCT, Literal
+
+REAL_DOMAIN = "real"
+LOG_DOMAIN = "log"
+
+
+class EvalError(ValueError):
+    """Shape or domain mismatch between circuit, weights, and traces (engine.py:30-31)."""
+
+
+# --------------------------------------------------------------------------
+# weights (engine.py:34-118)
+# --------------------------------------------------------------------------
+
+@dataclass
+class WeightAssignment:
+    """Per-input-slot values, one row per batch element."""
+
+    values: np.ndarray  # [batch, num_inputs]
+    domain: str = REAL_DOMAIN
+
+    def __post_init__(self) -> None:
+        self.values = np.atleast_2d(np.asarray(self.values, dtype=np.float64))
+        if self.values.ndim != 2 or self.values.shape[0] < 1:
+            raise EvalError("weights must be a [batch, num_inputs] matrix with batch >= 1")
+        if self.domain not in (REAL_DOMAIN, LOG_DOMAIN):
+            raise EvalError(f"unknown weight domain {self.domain!r}")
+        if self.domain == REAL_DOMAIN and not np.all(np.isfinite(self.values)):
+            raise EvalError("real-domain weights must be finite")
+        if self.domain == LOG_DOMAIN and np.any(self.values == np.inf):
+            raise EvalError("log-domain weights must be < +inf")
+
+    @property
+    def batch(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def num_inputs(self) -> int:
+        return self.values.shape[1]
+
+    def to_log(self) -> "WeightAssignment":
+        if self.domain == LOG_DOMAIN:
+            return self
+        with np.errstate(divide="ignore"):
+            return WeightAssignment(np.log(self.values), LOG_DOMAIN)
+
+
+def _code(lit) -> int:
+    return int(lit.to_dimacs())
+
+
+def weights_from_map(input_map: Mapping, per_literal: Mapping, domain: str = REAL_DOMAIN
+                     ) -> WeightAssignment:
+    """Single-row assignment from an explicit literal -> value map."""
+    by_code = {_code(k): float(v) for k, v in per_literal.items()}
+    row = np.empty(len(input_map), dtype=np.float64)
+    for lit, slot in input_map.items():
+        c = _code(lit)
+        if c not in by_code:
+            raise EvalError(f"missing weight for literal {lit}")
+        row[slot] = by_code[c]
+    return WeightAssignment(row[np.newaxis, :], domain)
+
+
+def weights_from_probabilities(input_map: Mapping, prob: Mapping[int, float]) -> WeightAssignment:
+    """Real weights from variable probabilities; the negative literal gets 1 - p."""
+    per = {}
+    for lit in input_map:
+        if lit.variable not in prob:
+            raise EvalError(f"missing probability for variable {lit.variable}")
+        p = float(prob[lit.variable])
+        per[Literal(lit.variable, lit.positive)] = p if lit.positive else 1.0 - p
+    return weights_from_map(input_map, per)
+
+
+def weights_from_json(payload, input_map: Mapping) -> WeightAssignment:
+    """``{"p": {...}}`` / ``{"w": {...}}`` objects, or a list of them (batched)."""
+    rows = payload if isinstance(payload, list) else [payload]
+    if not rows:
+        raise EvalError("weight file contains no rows")
+    out = []
+    for row in rows:
+        if not isinstance(row, dict) or len(row.keys() & {"p", "w"}) != 1:
+            raise EvalError("each weight row must have exactly one of 'p' or 'w'")
+        if "p" in row:
+            prob = {int(k): float(v) for k, v in row["p"].items()}
+            out.append(weights_from_probabilities(input_map, prob).values[0])
+        else:
+            per = {Literal.from_dimacs(int(k)): float(v) for k, v in row["w"].items()}
+            out.append(weights_from_map(input_map, per).values[0])
+    return WeightAssignment(np.stack(out), REAL_DOMAIN)
+
+
+# --------------------------------------------------------------------------
+# semirings (engine.py:158-193)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Semiring:
+    """Named semiring evaluated by the device kernels (``code`` = KLAY_*)."""
+
+    name: str
+    zero: float
+    one: float
+    code: int
+
+
+REAL = Semiring("real", 0.0, 1.0, _lib.KLAY_REAL)
+BOOLEAN = Semiring("bool", 0.0, 1.0, _lib.KLAY_BOOL)
+MAX_PRODUCT = Semiring("maxprod", 0.0, 1.0, _lib.KLAY_MAXPROD)
+SEMIRINGS = {s.name: s for s in (REAL, BOOLEAN, MAX_PRODUCT)}
+
+
+# --------------------------------------------------------------------------
+# device plan: the immutable per-circuit device state (engine._plans)
+# --------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _resolve_dtype(dtype):
+    if dtype is None:
+        return np.float64
+    dt = np.dtype(dtype)
+    if dt == np.float64:
+        return np.float64
+    if dt == np.float32:
+        return np.float32
+    raise EvalError(f"unsupported dtype {dt} (float32 or float64)")
+
+
+def _klay_dtype(np_dtype) -> int:
+    return _lib.KLAY_F64 if np.dtype(np_dtype) == np.float64 else _lib.KLAY_F32
+
+
+class DevicePlan:
+    """Device copy of a circuit's index vectors (CSR + transposed CSR).
+
+    Built once per (circuit, device) and cached on the circuit object like
+    the reference's ``tc._plans_cache`` (engine.py:138-155). Read-only after
+    creation; safe to share across streams.
+    """
+
+    def __init__(self, tc, device=None):
+        torch = _torch()
+        lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise _lib.KlayLibError("a CUDA device is required (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self.num_inputs = int(tc.num_inputs)
+        self.num_layers = len(tc.layers)
+        self.widths = [int(l.width) for l in tc.layers]
+        self.num_roots = int(tc.num_roots)
+        widths = np.array(self.widths, dtype=np.int64)
+        counts = np.array([len(l.sources) for l in tc.layers], dtype=np.int64)
+        for l, layer in enumerate(tc.layers, start=1):
+            expected = PRODUCT if l % 2 == 1 else "sum"
+            if layer.op != expected:
+                from .tensorized import KlayFormatError
+                raise KlayFormatError(f"layer {l} op {layer.op!r}, expected {expected!r}")
+        if self.num_layers:
+            src = np.ascontiguousarray(np.concatenate([np.asarray(l.sources, np.int64) for l in tc.layers]))
+            seg = np.ascontiguousarray(np.concatenate([np.asarray(l.segments, np.int64) for l in tc.layers]))
+        else:
+            src = seg = np.zeros(1, np.int64)
+        root_nodes = np.full(self.num_roots, -1, dtype=np.int64)
+        const_vals = np.zeros(max(self.num_roots, 1), dtype=np.int8)
+        free = [p for p in range(self.num_roots) if p not in tc.constant_roots]
+        if len(free) != len(tc.root_indices):
+            raise EvalError("root_indices and constant_roots do not add up to num_roots")
+        for p, r in zip(free, tc.root_indices):
+            root_nodes[p] = int(r)
+        for p, b in tc.constant_roots.items():
+            const_vals[p] = 1 if b else 0
+        root_nodes_buf = np.ascontiguousarray(root_nodes if self.num_roots else np.zeros(1, np.int64))
+        handle = ctypes.c_void_p()
+        rc = lib.klay_plan_create(
+            self.num_inputs, self.num_layers, widths.ctypes.data, counts.ctypes.data,
+            src.ctypes.data, seg.ctypes.data, self.num_roots, root_nodes_buf.ctypes.data,
+            const_vals.ctypes.data, self.device.index, ctypes.byref(handle))
+        _lib.check(rc, "klay_plan_create")
+        self._handle = handle
+        self._lib = lib
+        self.num_nodes = int(lib.klay_plan_num_nodes(handle))
+        self.max_width = int(lib.klay_plan_max_width(handle))
+        self.layer_offsets = [int(lib.klay_plan_layer_offset(handle, l))
+                              for l in range(self.num_layers + 1)]
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.klay_plan_destroy(h)
+            except Exception:
+                pass
+            self._handle = None
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def row_stride(self, batch: int, dtype) -> int:
+        return int(self._lib.klay_row_stride(batch, _klay_dtype(dtype)))
+
+    def _stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    # ---- device-resident entry points (torch tensors in / out) ----------
+    def alloc_values(self, batch: int, dtype, retain: bool = True):
+        torch = _torch()
+        ld = self.row_stride(batch, dtype)
+        rows = self.num_nodes if retain else 2 * self.max_width
+        tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        return torch.empty((rows, ld), dtype=tdt, device=self.device)
+
+    def forward(self, weights, semiring: int, dtype, retain=True, epsilon=0.0,
+                values=None, outputs=None):
+        """weights: cuda tensor [B, K] (float32/float64, semiring domain).
+        Returns (outputs [B, R] tensor, values buffer [rows, ld])."""
+        torch = _torch()
+        if weights.dim() != 2 or weights.shape[1] != self.num_inputs:
+            raise EvalError(f"weights have {weights.shape[-1]} columns, circuit expects {self.num_inputs}")
+        B = int(weights.shape[0])
+        if B < 1:
+            raise EvalError("batch must be >= 1")
+        if not weights.is_contiguous():
+            weights = weights.contiguous()
+        wdt = _lib.KLAY_F64 if weights.dtype == torch.float64 else _lib.KLAY_F32
+        if weights.dtype not in (torch.float32, torch.float64):
+            raise EvalError("weights must be float32 or float64")
+        if values is None:
+            values = self.alloc_values(B, dtype, retain)
+        ld = values.shape[1]
+        tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        if outputs is None:
+            outputs = torch.empty((B, self.num_roots), dtype=tdt, device=self.device)
+        rc = self._lib.klay_forward(
+            self._handle, semiring, _klay_dtype(dtype), weights.data_ptr(), wdt,
+            values.data_ptr(), ld, 1 if retain else 0,
+            outputs.data_ptr() if self.num_roots else None, B, float(epsilon), self._stream())
+        _lib.check(rc, "klay_forward")
+        return outputs, values
+
+    def workspace(self, batch: int, dtype):
+        torch = _torch()
+        ld = self.row_stride(batch, dtype)
+        nbytes = int(self._lib.klay_backward_workspace(self._handle, _klay_dtype(dtype), ld))
+        return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
+
+    def backward(self, values, batch: int, domain: int, dtype, seed=None, grads=None,
+                 workspace=None):
+        """values: retained trace buffer from forward(). seed: cuda [B, R] or
+        None (ones). Returns grads [B, K] tensor."""
+        torch = _torch()
+        tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        if grads is None:
+            grads = torch.empty((batch, self.num_inputs), dtype=tdt, device=self.device)
+        if workspace is None:
+            workspace = self.workspace(batch, dtype)
+        if seed is not None:
+            if tuple(seed.shape) != (batch, self.num_roots):
+                raise EvalError(f"seed must have shape {(batch, self.num_roots)}")
+            seed = seed.to(device=self.device, dtype=tdt).contiguous()
+        rc = self._lib.klay_backward(
+            self._handle, domain, _klay_dtype(dtype), values.data_ptr(), values.shape[1],
+            seed.data_ptr() if seed is not None else None,
+            grads.data_ptr() if self.num_inputs else None, workspace.data_ptr(), batch,
+            self._stream())
+        _lib.check(rc, "klay_backward")
+        return grads
+
+
+def device_plan(tc, device=None) -> DevicePlan:
+    """Cached DevicePlan of ``tc`` on ``device`` (default: current CUDA device)."""
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _lib.KlayLibError("a CUDA device is required (no CPU fallback)")
+    idx = torch.cuda.current_device() if device is None else (torch.device(device).index or 0)
+    cache = getattr(tc, "_klay_device_plans", None)
+    if cache is None:
+        cache = {}
+        try:
+            tc._klay_device_plans = cache
+        except AttributeError:
+            pass
+    plan = cache.get(idx)
+    if plan is None:
+        plan = DevicePlan(tc, torch.device("cuda", idx))
+        cache[idx] = plan
+    return plan
+
+
+# --------------------------------------------------------------------------
+# traces (engine.py:121-128)
+# --------------------------------------------------------------------------
+
+class _NodeValues(Sequence):
+    """Lazy host view of a device trace: item l is the [batch, width_l]
+    numpy matrix of layer l (0 = inputs), copied on first access."""
+
+    def __init__(self, plan: DevicePlan, values, batch: int):
+        self._plan, self._values, self._batch = plan, values, batch
+        self._cache = {}
+
+    def __len__(self):
+        return self._plan.num_layers + 1
+
+    def __getitem__(self, l):
+        if isinstance(l, slice):
+            return [self[i] for i in range(*l.indices(len(self)))]
+        if l < 0:
+            l += len(self)
+        if not 0 <= l < len(self):
+            raise IndexError(l)
+        if l not in self._cache:
+            start = self._plan.layer_offsets[l]
+            w = self._plan.num_inputs if l == 0 else self._plan.widths[l - 1]
+            block = self._values[start:start + w, :self._batch]
+            self._cache[l] = block.t().contiguous().cpu().numpy()
+        return self._cache[l]
+
+
+@dataclass
+class EvalTrace:
+    """Forward-pass record: per-layer node values (when retained) and root outputs."""
+
+    domain: str
+    outputs: np.ndarray  # [batch, num_roots]
+    node_values: Sequence | None  # [batch, width_l] per layer 0..L
+    epsilon: float = 0.0
+    _device_values: object = field(default=None, repr=False)
+    _plan: object = field(default=None, repr=False)
+    _dtype: object = field(default=None, repr=False)
+
+
+# --------------------------------------------------------------------------
+# reference-facing API (engine.py:196-384)
+# --------------------------------------------------------------------------
+
+def _check_shapes(tc, weights: WeightAssignment) -> None:
+    if weights.num_inputs != tc.num_inputs:
+        raise EvalError(
+            f"weights have {weights.num_inputs} columns, circuit expects {tc.num_inputs}")
+
+
+def _run(tc, values: np.ndarray, code: int, dtype, retain: bool, epsilon: float = 0.0):
+    torch = _torch()
+    plan = device_plan(tc)
+    w = torch.from_numpy(np.ascontiguousarray(values)).to(plan.device, non_blocking=True)
+    out, buf = plan.forward(w, code, dtype, retain=retain, epsilon=epsilon)
+    return plan, out.cpu().numpy(), buf
+
+
+def forward_real(tc, weights: WeightAssignment, retain_trace: bool = True, dtype=None) -> EvalTrace:
+    """Evaluate in the real semiring; returns the trace with root outputs."""
+    if weights.domain != REAL_DOMAIN:
+        raise EvalError("forward_real requires real-domain weights")
+    _check_shapes(tc, weights)
+    dt = _resolve_dtype(dtype)
+    plan, out, buf = _run(tc, weights.values, _lib.KLAY_REAL, dt, retain_trace)
+    nv = _NodeValues(plan, buf, weights.batch) if retain_trace else None
+    return EvalTrace(REAL_DOMAIN, out, nv, 0.0, buf if retain_trace else None, plan, dt)
+
+
+def forward_log(tc, weights: WeightAssignment, epsilon: float = 0.0, retain_trace: bool = True,
+                dtype=None) -> EvalTrace:
+    """Log semiring: products are sums, sums a max-trick logsumexp; all -inf
+    segments give -inf, never NaN; ``epsilon`` is added inside the log."""
+    if weights.domain != LOG_DOMAIN:
+        raise EvalError("forward_log requires log-domain weights")
+    if epsilon < 0:
+        raise EvalError("epsilon must be >= 0")
+    _check_shapes(tc, weights)
+    dt = _resolve_dtype(dtype)
+    plan, out, buf = _run(tc, weights.values, _lib.KLAY_LOG, dt, retain_trace, epsilon)
+    nv = _NodeValues(plan, buf, weights.batch) if retain_trace else None
+    return EvalTrace(LOG_DOMAIN, out, nv, epsilon, buf if retain_trace else None, plan, dt)
+
+
+def evaluate_semiring(tc, weights: WeightAssignment, semiring) -> np.ndarray:
+    """Forward evaluation under a named semiring; returns [batch, roots]."""
+    if isinstance(semiring, str):
+        if semiring == "log":
+            return forward_log(tc, weights.to_log(), retain_trace=False).outputs
+        if semiring not in SEMIRINGS:
+            raise EvalError(f"unknown semiring {semiring!r}")
+        semiring = SEMIRINGS[semiring]
+    if not isinstance(semiring, Semiring) or semiring.name not in SEMIRINGS:
+        raise EvalError(f"unsupported semiring {getattr(semiring, 'name', semiring)!r}")
+    _check_shapes(tc, weights)
+    _, out, _ = _run(tc, weights.values, semiring.code, np.float64, False)
+    return out
+
+
+def _upload_trace(tc, trace, plan):
+    """Device trace from a host trace (e.g. a reference EvalTrace)."""
+    torch = _torch()
+    nv = trace.node_values
+    dt = np.float64 if nv[0].dtype == np.float64 else np.float32
+    batch = nv[0].shape[0]
+    buf = plan.alloc_values(batch, dt, retain=True)
+    for l, m in enumerate(nv):
+        start = plan.layer_offsets[l]
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(m, dtype=dt).T)).to(plan.device)
+        buf[start:start + t.shape[0], :batch].copy_(t)
+    return buf, dt
+
+
+def backward(tc, trace: EvalTrace, seed: np.ndarray | None = None) -> np.ndarray:
+    """Gradient of ``sum_r seed[:, r] * root_r`` w.r.t. the input slots
+    (engine.py:307-355); zero-safe product adjoints in the real domain."""
+    torch = _torch()
+    if trace.node_values is None:
+        raise EvalError("backward requires a trace with retain_trace=True")
+    if len(trace.node_values) != len(tc.layers) + 1:
+        raise EvalError("trace does not match circuit layer count")
+    plan = device_plan(tc)
+    buf = getattr(trace, "_device_values", None)
+    if buf is None or getattr(trace, "_plan", None) is not plan:
+        buf, dt = _upload_trace(tc, trace, plan)
+        batch = trace.node_values[0].shape[0]
+    else:
+        dt = trace._dtype
+        batch = trace.outputs.shape[0]
+    if seed is not None:
+        seed = np.asarray(seed, dtype=dt)
+        if seed.shape != (batch, tc.num_roots):
+            raise EvalError(f"seed must have shape {(batch, tc.num_roots)}")
+        seed = torch.from_numpy(np.ascontiguousarray(seed)).to(plan.device, non_blocking=True)
+    domain = _lib.KLAY_LOG if trace.domain == LOG_DOMAIN else _lib.KLAY_REAL
+    grads = plan.backward(buf, batch, domain, dt, seed=seed)
+    return grads.cpu().numpy()
+
+
+def gradient(tc, weights: WeightAssignment, log_domain: bool = False, epsilon: float = 0.0,
+             seed: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Forward + backward; returns (outputs, input grads) (engine.py:372-384)."""
+    if log_domain:
+        trace = forward_log(tc, weights.to_log(), epsilon=epsilon)
+    else:
+        trace = forward_real(tc, weights)
+    return trace.outputs, backward(tc, trace, seed)
