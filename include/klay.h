@@ -97,11 +97,17 @@ int64_t klay_row_stride(int64_t batch, int32_t dtype);
  *                2 * max_width rows (ping-pong, only the last layer survives)
  *   outputs      device [B, R] row-major, element type `dtype` (may be NULL)
  *   epsilon      log semiring only, added inside the log (must be >= 0)
+ *   workspace    device scratch of klay_forward_workspace() bytes (may be
+ *                NULL when that is 0: no segment needs a split reduction)
  */
 int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
                  const void* weights, int32_t weights_dtype, void* values, int64_t ld,
                  int32_t retain, void* outputs, int64_t batch, double epsilon,
-                 void* stream);
+                 void* workspace, void* stream);
+
+/* Scratch bytes klay_forward needs for row stride `ld` (leaf partials of
+ * segments longer than 129 edges, split in numpy pairwise-tree order). */
+size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 
 /*
  * Backward pass over a retained trace. Replaces engine.backward

@@ -33,7 +33,8 @@ SIGNATURES = {
     "klay_plan_layer_offset": (_c_i64, [_vp, _c_i32]),
     "klay_row_stride": (_c_i64, [_c_i64, _c_i32]),
     "klay_forward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i32, _vp, _c_i64, _c_i32, _vp,
-                                    _c_i64, ctypes.c_double, _vp]),
+                                    _c_i64, ctypes.c_double, _vp, _vp]),
+    "klay_forward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
     "klay_backward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _vp, _vp, _vp, _c_i64, _vp]),
     "klay_backward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
     "klay_launch_count": (_c_i64, []),

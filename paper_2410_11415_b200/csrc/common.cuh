@@ -1,0 +1,221 @@
+// Shared device helpers of libklay: 16-byte value vectors, numpy-faithful
+// elementwise ops and the streaming segment reducers.
+//
+// A "segment" is one node's incoming edge list in CSR order (forward:
+// parent <- children; backward: child <- parents over the transposed CSR).
+// Reducers consume the segment's edge values strictly in edge order, so the
+// result reproduces the reference's reduction order:
+//   SumOp   np.add.reduceat        x0 + pairwise(x[1:])   (bit-exact)
+//   ProdOp  np.multiply.reduceat   sequential              (bit-exact)
+//   MaxOp / MinOp  np.maximum / np.minimum.reduceat, NaN-propagating
+//   LseOp   _segment_logsumexp (engine.py:274-282), merged online; equal to
+//           the two-pass form bit-for-bit for fan-in <= 2, ulp-close beyond
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace klay {
+
+enum { SR_REAL = 0, SR_LOG = 1, SR_BOOL = 2, SR_MAXPROD = 3 };
+enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2 };
+// reduction kinds
+enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4 };
+
+// numpy's pairwise summation works on blocks of at most this many elements
+constexpr int PW_BLOCK = 128;
+
+template <typename T>
+struct alignas(16) Vec {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+
+__device__ __forceinline__ Vec<float> ldv(const float* p) {
+  float4 u = __ldg(reinterpret_cast<const float4*>(p));
+  Vec<float> r;
+  r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
+  return r;
+}
+__device__ __forceinline__ Vec<double> ldv(const double* p) {
+  double2 u = __ldg(reinterpret_cast<const double2*>(p));
+  Vec<double> r;
+  r.v[0] = u.x; r.v[1] = u.y;
+  return r;
+}
+__device__ __forceinline__ void stv(float* p, const Vec<float>& r) {
+  *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+}
+__device__ __forceinline__ void stv(double* p, const Vec<double>& r) {
+  *reinterpret_cast<double2*>(p) = make_double2(r.v[0], r.v[1]);
+}
+
+template <typename T>
+__device__ __forceinline__ Vec<T> vfill(T x) {
+  Vec<T> r;
+#pragma unroll
+  for (int k = 0; k < Vec<T>::N; ++k) r.v[k] = x;
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ Vec<T> vadd(const Vec<T>& a, const Vec<T>& b) {
+  Vec<T> r;
+#pragma unroll
+  for (int k = 0; k < Vec<T>::N; ++k) r.v[k] = a.v[k] + b.v[k];
+  return r;
+}
+
+__device__ __forceinline__ float kexp(float x) { return expf(x); }
+__device__ __forceinline__ double kexp(double x) { return exp(x); }
+__device__ __forceinline__ float klog(float x) { return logf(x); }
+__device__ __forceinline__ double klog(double x) { return log(x); }
+
+// np.maximum / np.minimum: NaN-propagating.
+template <typename T>
+__device__ __forceinline__ T npmax(T a, T b) { return (a > b || a != a) ? a : b; }
+template <typename T>
+__device__ __forceinline__ T npmin(T a, T b) { return (a < b || a != a) ? a : b; }
+
+// ---------------------------------------------------------------------------
+// streaming reducers: begin(n) for a whole segment of n >= 1 edges,
+// begin_leaf(len) for one pairwise leaf of the segment's tail (no x0),
+// push(x) per edge in order, result() / partial()
+// ---------------------------------------------------------------------------
+template <typename T>
+struct SumOp {
+  // The 8 pairwise accumulators live in shared memory (slot q of this thread
+  // at r[q * rstride]); they are only touched by segments with more than 8
+  // tail elements, so keeping them out of registers keeps occupancy up.
+  Vec<T> x0, acc;
+  Vec<T>* r;
+  int rstride;
+  int k, m, mainend;
+  __device__ __forceinline__ void start(int k0, int len) {
+    k = k0;
+    m = len;
+    mainend = len - (len & 7);
+    acc = vfill<T>(T(-0.0));
+  }
+  __device__ __forceinline__ void begin(int n) { start(0, n - 1); }
+  __device__ __forceinline__ void begin_leaf(int len) { start(1, len); }
+  __device__ __forceinline__ Vec<T> combine8() const {
+    Vec<T> q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = r[i * rstride];
+    Vec<T> res;
+#pragma unroll
+    for (int c = 0; c < Vec<T>::N; ++c)
+      res.v[c] = ((q[0].v[c] + q[1].v[c]) + (q[2].v[c] + q[3].v[c])) +
+                 ((q[4].v[c] + q[5].v[c]) + (q[6].v[c] + q[7].v[c]));
+    return res;
+  }
+  __device__ __forceinline__ void push(const Vec<T>& x) {
+    if (k == 0) {
+      x0 = x;
+    } else {
+      const int j = k - 1;
+      if (m < 8) {
+        acc = vadd(acc, x);
+      } else if (j < mainend) {
+        Vec<T>& slot = r[(j & 7) * rstride];
+        slot = (j < 8) ? x : vadd(slot, x);
+      } else {
+        if (j == mainend) acc = combine8();
+        acc = vadd(acc, x);
+      }
+    }
+    ++k;
+  }
+  // pairwise sum of the elements after x0 (or of the leaf)
+  __device__ __forceinline__ Vec<T> partial() const {
+    if (m < 8 || mainend < m) return acc;
+    return combine8();
+  }
+  __device__ __forceinline__ Vec<T> result() const { return m == 0 ? x0 : vadd(x0, partial()); }
+};
+
+template <typename T, int RK>
+struct SeqOp {  // RK_PROD / RK_MAX / RK_MIN: strictly sequential
+  Vec<T> acc;
+  int k;
+  __device__ __forceinline__ void begin(int) { k = 0; }
+  __device__ __forceinline__ void begin_leaf(int) { k = 0; }
+  __device__ __forceinline__ void push(const Vec<T>& x) {
+    if (k == 0) {
+      acc = x;
+    } else {
+#pragma unroll
+      for (int c = 0; c < Vec<T>::N; ++c) {
+        if constexpr (RK == RK_PROD) acc.v[c] = acc.v[c] * x.v[c];
+        else if constexpr (RK == RK_MAX) acc.v[c] = npmax(acc.v[c], x.v[c]);
+        else acc.v[c] = npmin(acc.v[c], x.v[c]);
+      }
+    }
+    ++k;
+  }
+  __device__ __forceinline__ Vec<T> partial() const { return acc; }
+  __device__ __forceinline__ Vec<T> result() const { return acc; }
+};
+
+template <typename T>
+__device__ __forceinline__ void lse_merge(T& m, T& t, T m2, T t2) {
+  if (m2 > m) {
+    t = t * kexp(m - m2) + t2;
+    m = m2;
+  } else if (m2 == -INFINITY) {
+    // contributes nothing (an all -inf part is masked to 0, engine.py:279)
+  } else {
+    t = t + t2 * kexp(m2 - m);
+  }
+}
+
+template <typename T>
+struct LseOp {
+  Vec<T> m, t;
+  T eps;
+  __device__ __forceinline__ void begin(int) {
+    m = vfill<T>(T(-INFINITY));
+    t = vfill<T>(T(0));
+  }
+  __device__ __forceinline__ void begin_leaf(int n) { begin(n); }
+  __device__ __forceinline__ void push(const Vec<T>& x) {
+#pragma unroll
+    for (int c = 0; c < Vec<T>::N; ++c) {
+      const T xv = x.v[c];
+      if (xv > m.v[c]) {
+        t.v[c] = t.v[c] * kexp(m.v[c] - xv) + T(1);
+        m.v[c] = xv;
+      } else if (xv != T(-INFINITY)) {
+        t.v[c] = t.v[c] + kexp(xv - m.v[c]);
+      }
+    }
+  }
+  __device__ __forceinline__ Vec<T> result() const {
+    Vec<T> r;
+#pragma unroll
+    for (int c = 0; c < Vec<T>::N; ++c) {
+      const T res = klog(t.v[c] + eps) + m.v[c];
+      r.v[c] = (m.v[c] == T(-INFINITY)) ? T(-INFINITY) : res;
+    }
+    return r;
+  }
+};
+
+// pairwise-tree combination of leaf partials stored one row apart
+// (same recursion as numpy's pairwise_sum above PW_BLOCK elements)
+template <typename T>
+__device__ Vec<T> tree_sum(const T* leaves, long long stride, int& leaf, int len) {
+  if (len <= PW_BLOCK) {
+    Vec<T> v = ldv(leaves + (size_t)leaf * stride);
+    ++leaf;
+    return v;
+  }
+  int n2 = len / 2;
+  n2 -= n2 % 8;
+  Vec<T> a = tree_sum(leaves, stride, leaf, n2);
+  Vec<T> b = tree_sum(leaves, stride, leaf, len - n2);
+  return vadd(a, b);
+}
+
+}  // namespace klay

@@ -1,0 +1,24 @@
+// Forward layer kernels for float (explicit instantiations).
+#include "layer_kernels.cuh"
+
+namespace klay {
+
+int launch_forward_layer(int sr, bool prod, const LayerArgs<float>& a, cudaStream_t s) {
+  using G = FwdGather<float>;
+  switch (sr) {
+    case SR_REAL:
+      if (prod) return launch_layer<float, RK_PROD, G>(a, s);
+      else return launch_layer<float, RK_SUM, G>(a, s);
+    case SR_LOG:
+      if (prod) return launch_layer<float, RK_SUM, G>(a, s);
+      else return launch_layer<float, RK_LSE, G>(a, s);
+    case SR_BOOL:
+      if (prod) return launch_layer<float, RK_MIN, G>(a, s);
+      else return launch_layer<float, RK_MAX, G>(a, s);
+    default:  // max-product
+      if (prod) return launch_layer<float, RK_PROD, G>(a, s);
+      else return launch_layer<float, RK_MAX, G>(a, s);
+  }
+}
+
+}  // namespace klay

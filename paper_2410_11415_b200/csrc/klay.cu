@@ -6,21 +6,41 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
 
-#include "kernels.cuh"
+#include "layer_api.h"
 
 using namespace klay;
 
 namespace {
 
+enum { SR_REAL_ = 0, SR_LOG_ = 1 };
+enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2 };
+
+// work-item shape (see layer_kernels.cuh)
+constexpr int ITEM_EDGES = 64;   // edges per range item
+constexpr int ITEM_NODES = 31;   // nodes per range item (one lane per segment end)
+constexpr int PW_BLOCK_H = 128;  // numpy pairwise block; longer tails are split
+
 thread_local std::string g_err;
 
-// Kernel launches issued by this library (all threads), for the benchmark's
-// gpu_launches claim.
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define KLAY_CUDA(call)                                                          \
+  do {                                                                           \
+    cudaError_t e_ = (call);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(KLAY_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Kernel launches issued by this library (all threads).
 std::atomic<long long> g_launches{0};
 
 // Optional per-launch event timing (klay_profiler_begin / _end).
@@ -36,7 +56,6 @@ struct LaunchScope {
   int kind, layer;
   cudaEvent_t a = nullptr, b = nullptr;
   LaunchScope(cudaStream_t s_, int kind_, int layer_) : s(s_), kind(kind_), layer(layer_) {
-    ++g_launches;
     if (g_prof_on) {
       cudaEventCreate(&a);
       cudaEventCreate(&b);
@@ -51,17 +70,57 @@ struct LaunchScope {
   }
 };
 
-int fail(int code, const std::string& msg) {
-  g_err = msg;
-  return code;
+struct ItemSet {
+  std::vector<int4> items;
+  std::vector<int4> heavy;
+  int slots = 0;
+};
+
+void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
+  if (len <= PW_BLOCK_H) {
+    out.push_back({a, a + len});
+    return;
+  }
+  int n2 = len / 2;
+  n2 -= n2 % 8;
+  split_leaves(a, n2, out);
+  split_leaves(a + n2, len - n2, out);
 }
 
-#define KLAY_CUDA(call)                                                          \
-  do {                                                                           \
-    cudaError_t e_ = (call);                                                     \
-    if (e_ != cudaSuccess)                                                       \
-      return fail(KLAY_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
-  } while (0)
+// Balanced work items over one CSR (W segments, offsets off[base..base+W]).
+void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s) {
+  std::vector<int4> leaves, singles, ranges;
+  std::vector<std::pair<int, int>> lv;
+  int rb = -1, re_edges = 0;
+  auto flush = [&](int end_node) {
+    if (rb >= 0 && end_node > rb)
+      ranges.push_back(make_int4(rb, end_node, off[base + rb], off[base + end_node]));
+    rb = -1;
+    re_edges = 0;
+  };
+  for (int p = 0; p < W; ++p) {
+    const int s0 = off[base + p], n = off[base + p + 1] - s0;
+    if (n - 1 > PW_BLOCK_H) {
+      flush(p);
+      lv.clear();
+      split_leaves(s0 + 1, n - 1, lv);
+      s.heavy.push_back(make_int4(p, s.slots, (int)lv.size(), 0));
+      for (auto& l : lv) leaves.push_back(make_int4(p, -(s.slots++) - 1, l.first, l.second));
+    } else if (n > ITEM_EDGES) {
+      flush(p);
+      singles.push_back(make_int4(p, p + 1, s0, s0 + n));
+    } else {
+      if (rb >= 0 && (p - rb >= ITEM_NODES || re_edges + n > ITEM_EDGES)) flush(p);
+      if (rb < 0) rb = p;
+      re_edges += n;
+    }
+  }
+  flush(W);
+  s.items.reserve(leaves.size() + singles.size() + ranges.size());
+  s.items.insert(s.items.end(), leaves.begin(), leaves.end());
+  s.items.insert(s.items.end(), singles.begin(), singles.end());
+  s.items.insert(s.items.end(), ranges.begin(), ranges.end());
+}
 
 struct LayerDesc {
   int64_t W, Wprev, E;
@@ -70,6 +129,8 @@ struct LayerDesc {
   int64_t off_base;       // into off[] (W+1 entries per layer)
   int64_t e_base;         // into src[] / tpar[]
   int64_t toff_base;      // into toff[] (Wprev+1 entries per layer)
+  int64_t fi_base, fi_n, fh_base, fh_n, f_slots;  // forward items / heavy
+  int64_t bi_base, bi_n, bh_base, bh_n, b_slots;  // backward items / heavy
 };
 
 struct DeviceGuard {
@@ -94,13 +155,15 @@ struct KlayPlan {
   int32_t R = 0;
   int64_t total_rows = 0;
   int64_t max_width = 0;
-  int64_t max_fanin = 0;
+  int64_t max_fslots = 0, max_bslots = 0;
   std::vector<LayerDesc> layers;
   std::vector<int64_t> layer_row;  // L+1 entries
   int* d_off = nullptr;
   int* d_src = nullptr;
   int* d_toff = nullptr;
   int* d_tpar = nullptr;
+  int4* d_items = nullptr;
+  int4* d_heavy = nullptr;
   int* d_root_node = nullptr;
   signed char* d_const = nullptr;
   int* d_top_off = nullptr;
@@ -108,7 +171,7 @@ struct KlayPlan {
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
 };
 
-extern "C" const char* klay_version(void) { return "libklay 0.1 sm_100a"; }
+extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
 
 extern "C" const char* klay_last_error(void) { return g_err.c_str(); }
 
@@ -118,6 +181,8 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_src);
   cudaFree(p->d_toff);
   cudaFree(p->d_tpar);
+  cudaFree(p->d_items);
+  cudaFree(p->d_heavy);
   cudaFree(p->d_root_node);
   cudaFree(p->d_const);
   cudaFree(p->d_top_off);
@@ -145,6 +210,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   if (num_layers > 0 && (!widths || !edge_counts || !sources || !segments))
     return fail(KLAY_EINVAL, "NULL layer arrays");
   if (num_roots > 0 && (!root_nodes || !const_vals)) return fail(KLAY_EINVAL, "NULL root arrays");
+  if (num_inputs >= (1LL << 31)) return fail(KLAY_EINVAL, "too many inputs for int32 indexing");
 
   KlayPlan* p = new KlayPlan();
   p->device = device;
@@ -153,23 +219,25 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   p->R = num_roots;
 
   std::vector<int> off, src, toff, tpar;
+  std::vector<int4> items, heavy;
   int64_t prev_w = num_inputs, row = num_inputs, e_base = 0;
   p->max_width = num_inputs;
   p->layer_row.push_back(0);
+  auto bad = [&](int code, const std::string& m) {
+    plan_free(p);
+    return fail(code, m);
+  };
   for (int32_t l = 0; l < num_layers; ++l) {
     const int64_t W = widths[l], E = edge_counts[l];
     const int64_t* S = sources + e_base;
     const int64_t* G = segments + e_base;
-    char where[64];
-    snprintf(where, sizeof where, "layer %d: ", l + 1);
+    const std::string where = "layer " + std::to_string(l + 1) + ": ";
     // invariants of tensorize.py:105-125
-    if (W <= 0) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "nonpositive width"); }
-    if (E <= 0) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "no edges"); }
-    if (W >= (1LL << 31) || E >= (1LL << 31) || prev_w >= (1LL << 31)) {
-      plan_free(p);
-      return fail(KLAY_EINVAL, std::string(where) + "layer exceeds int32 indexing");
-    }
-    LayerDesc d;
+    if (W <= 0) return bad(KLAY_EFORMAT, where + "nonpositive width");
+    if (E <= 0) return bad(KLAY_EFORMAT, where + "no edges");
+    if (W >= (1LL << 31) || E >= (1LL << 31) || (int64_t)src.size() + E >= (1LL << 31))
+      return bad(KLAY_EINVAL, where + "exceeds int32 indexing");
+    LayerDesc d{};
     d.W = W; d.Wprev = prev_w; d.E = E; d.prod = (l % 2 == 0);
     d.row = row; d.prev_row = row - prev_w;
     d.off_base = (int64_t)off.size();
@@ -178,17 +246,16 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     // CSR offsets of the parent segments (engine.py:144-146)
     std::vector<int64_t> cnt(W, 0), gcnt(prev_w, 0);
     for (int64_t e = 0; e < E; ++e) {
-      if (e > 0 && G[e] < G[e - 1]) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "aggregation indices not nondecreasing"); }
-      if (G[e] < 0 || G[e] >= W) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "aggregation indices must cover 0..width-1"); }
-      if (S[e] < 0 || S[e] >= prev_w) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "edge index out of range"); }
+      if (e > 0 && G[e] < G[e - 1]) return bad(KLAY_EFORMAT, where + "aggregation indices not nondecreasing");
+      if (G[e] < 0 || G[e] >= W) return bad(KLAY_EFORMAT, where + "aggregation indices must cover 0..width-1");
+      if (S[e] < 0 || S[e] >= prev_w) return bad(KLAY_EFORMAT, where + "edge index out of range");
       ++cnt[G[e]];
       ++gcnt[S[e]];
     }
     off.push_back(0);
     int64_t acc = 0;
     for (int64_t i = 0; i < W; ++i) {
-      if (cnt[i] == 0) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "aggregation indices must cover 0..width-1"); }
-      p->max_fanin = std::max(p->max_fanin, cnt[i]);
+      if (cnt[i] == 0) return bad(KLAY_EFORMAT, where + "aggregation indices must cover 0..width-1");
       acc += cnt[i];
       off.push_back((int)acc);
     }
@@ -199,7 +266,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     toff.push_back(0);
     acc = 0;
     for (int64_t j = 0; j < prev_w; ++j) {
-      if (gcnt[j] == 0) { plan_free(p); return fail(KLAY_EFORMAT, std::string(where) + "some previous-layer node is never read"); }
+      if (gcnt[j] == 0) return bad(KLAY_EFORMAT, where + "some previous-layer node is never read");
       pos[j] = acc;
       acc += gcnt[j];
       toff.push_back((int)acc);
@@ -207,6 +274,26 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     const size_t tb = tpar.size();
     tpar.resize(tb + E);
     for (int64_t e = 0; e < E; ++e) tpar[tb + pos[S[e]]++] = (int)G[e];
+    // work items: forward over parents, backward over children
+    ItemSet fs, bs;
+    build_items(off, (size_t)d.off_base, (int)W, fs);
+    build_items(toff, (size_t)d.toff_base, (int)prev_w, bs);
+    d.fi_base = (int64_t)items.size();
+    d.fi_n = (int64_t)fs.items.size();
+    items.insert(items.end(), fs.items.begin(), fs.items.end());
+    d.bi_base = (int64_t)items.size();
+    d.bi_n = (int64_t)bs.items.size();
+    items.insert(items.end(), bs.items.begin(), bs.items.end());
+    d.fh_base = (int64_t)heavy.size();
+    d.fh_n = (int64_t)fs.heavy.size();
+    heavy.insert(heavy.end(), fs.heavy.begin(), fs.heavy.end());
+    d.bh_base = (int64_t)heavy.size();
+    d.bh_n = (int64_t)bs.heavy.size();
+    heavy.insert(heavy.end(), bs.heavy.begin(), bs.heavy.end());
+    d.f_slots = fs.slots;
+    d.b_slots = bs.slots;
+    p->max_fslots = std::max<int64_t>(p->max_fslots, fs.slots);
+    p->max_bslots = std::max<int64_t>(p->max_bslots, bs.slots);
     p->layers.push_back(d);
     p->layer_row.push_back(row);
     p->max_width = std::max(p->max_width, W);
@@ -224,10 +311,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   for (int32_t q = 0; q < num_roots; ++q) {
     rn[q] = (int)root_nodes[q];
     cv[q] = const_vals[q] ? 1 : 0;
-    if (root_nodes[q] >= prev_w || root_nodes[q] < -1) {
-      plan_free(p);
-      return fail(KLAY_EFORMAT, "root index outside final layer");
-    }
+    if (root_nodes[q] >= prev_w || root_nodes[q] < -1)
+      return bad(KLAY_EFORMAT, "root index outside final layer");
     if (root_nodes[q] >= 0) by_node[root_nodes[q]].push_back(q);
   }
   std::vector<int> top_off(1, 0), top_pos;
@@ -240,6 +325,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   int rc;
   if ((rc = upload(&p->d_off, off)) || (rc = upload(&p->d_src, src)) ||
       (rc = upload(&p->d_toff, toff)) || (rc = upload(&p->d_tpar, tpar)) ||
+      (rc = upload(&p->d_items, items)) || (rc = upload(&p->d_heavy, heavy)) ||
       (rc = upload(&p->d_root_node, rn)) || (rc = upload(&p->d_const, cv)) ||
       (rc = upload(&p->d_top_off, top_off)) || (rc = upload(&p->d_top_pos, top_pos))) {
     plan_free(p);
@@ -269,77 +355,68 @@ extern "C" int64_t klay_row_stride(int64_t batch, int32_t dtype) {
   return (batch + per16 - 1) / per16 * per16;
 }
 
-namespace {
+static size_t esize(int32_t dtype) { return dtype == KLAY_F64 ? 8 : 4; }
 
-struct Launch {
-  dim3 grid, block;
-};
-
-// threads -> (row, 16-byte vector); block of 256 = vx vectors x ny rows
-Launch row_launch(int64_t rows, int V) {
-  int vx = 1;
-  while (vx < V && vx < 256) vx <<= 1;
-  const int ny = 256 / vx;
-  Launch L;
-  L.block = dim3(vx, ny, 1);
-  L.grid = dim3((unsigned)((rows + ny - 1) / ny), (unsigned)((V + vx - 1) / vx), 1);
-  return L;
+extern "C" size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
+  if (!plan) return 0;
+  // heavy-segment leaf partials; LSE keeps (max, sum) pairs
+  return (size_t)2 * plan->max_fslots * ld * esize(dtype);
 }
 
-template <typename T, int SR>
-void launch_fwd_layer(const FwdArgs<T>& a, bool prod, cudaStream_t s) {
-  Launch L = row_launch(a.W, a.V);
-  if (prod)
-    fwd_layer_kernel<T, SR, true><<<L.grid, L.block, 0, s>>>(a);
-  else
-    fwd_layer_kernel<T, SR, false><<<L.grid, L.block, 0, s>>>(a);
+extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
+  if (!plan) return 0;
+  return ((size_t)2 * plan->max_width + plan->max_bslots) * ld * esize(dtype);
+}
+
+namespace {
+
+template <typename T>
+LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, int64_t ld) {
+  LayerArgs<T> a{};
+  a.items = p->d_items + (fwd ? d.fi_base : d.bi_base);
+  a.n_items = (int)(fwd ? d.fi_n : d.bi_n);
+  a.heavy = p->d_heavy + (fwd ? d.fh_base : d.bh_base);
+  a.n_heavy = (int)(fwd ? d.fh_n : d.bh_n);
+  a.off = fwd ? p->d_off + d.off_base : p->d_toff + d.toff_base;
+  a.idx = fwd ? p->d_src + d.e_base : p->d_tpar + d.e_base;
+  a.V = V;
+  a.ld = ld;
+  a.foff = p->d_off + d.off_base;
+  a.fsrc = p->d_src + d.e_base;
+  return a;
 }
 
 template <typename T>
 int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* values, int64_t ld,
-                 bool retain, T* outputs, int64_t B, double eps, cudaStream_t s) {
+                 bool retain, T* outputs, int64_t B, double eps, T* work, cudaStream_t s) {
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* pingpong[2] = {values, values + (size_t)p->max_width * ld};
-  // inputs -> rows 0..K-1 (node-major), identity padding
-  T pad = (sr == SR_LOG) ? T(0) : T(1);
+  const T pad = (sr == SR_LOG_) ? T(0) : T(1);
   if (p->K > 0) {
-    dim3 grid((unsigned)((ld + 31) / 32), (unsigned)((p->K + 31) / 32));
-    dim3 block(32, 8);
     LaunchScope ls(s, 2, 0);
-    if (wdt == KLAY_F64)
-      load_inputs_kernel<T, double><<<grid, block, 0, s>>>((const double*)weights, values, (int)p->K, B, ld, pad);
-    else
-      load_inputs_kernel<T, float><<<grid, block, 0, s>>>((const float*)weights, values, (int)p->K, B, ld, pad);
+    launch_load_inputs<T>(weights, wdt == KLAY_F64, values, (int)p->K, B, ld, pad, s);
+    ++g_launches;
   }
   const T* prev = values;
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
-    FwdArgs<T> a;
+    LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
+    a.out = cur;
     a.prev = prev;
-    a.cur = cur;
-    a.off = p->d_off + d.off_base;
-    a.src = p->d_src + d.e_base;
-    a.W = (int)d.W;
-    a.V = V;
-    a.ld = ld;
     a.eps = (T)eps;
+    a.scratch = work;
+    a.tpart = (long long)p->max_fslots * ld;
     LaunchScope ls(s, 0, l + 1);
-    switch (sr) {
-      case SR_REAL: launch_fwd_layer<T, SR_REAL>(a, d.prod, s); break;
-      case SR_LOG: launch_fwd_layer<T, SR_LOG>(a, d.prod, s); break;
-      case SR_BOOL: launch_fwd_layer<T, SR_BOOL>(a, d.prod, s); break;
-      default: launch_fwd_layer<T, SR_MAXPROD>(a, d.prod, s); break;
-    }
+    g_launches += launch_forward_layer(sr, d.prod, a, s);
     prev = cur;
   }
-  if (outputs && p->R > 0 && B > 0) {
-    const T zero = (sr == SR_LOG) ? T(-INFINITY) : T(0);
-    const T one = (sr == SR_LOG) ? T(0) : T(1);
-    const int64_t n = B * p->R;
+  if (outputs && p->R > 0) {
+    const T zero = (sr == SR_LOG_) ? T(-INFINITY) : T(0);
+    const T one = (sr == SR_LOG_) ? T(0) : T(1);
     LaunchScope ls(s, 2, p->L + 1);
-    assemble_outputs_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-        prev, p->d_root_node, p->d_const, outputs, p->R, B, ld, zero, one);
+    launch_assemble_outputs<T>(prev, p->d_root_node, p->d_const, outputs, p->R, B, ld, zero, one, s);
+    ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());
   return KLAY_OK;
@@ -350,43 +427,43 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
                   T* grads, T* work, int64_t B, cudaStream_t s) {
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* g[2] = {work, work + (size_t)p->max_width * ld};
+  T* scratch = work + (size_t)2 * p->max_width * ld;
   int cur = 0;
   {
-    const int64_t n = p->WL * ld;
     LaunchScope ls(s, 3, p->L + 1);
-    seed_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, p->d_top_off, p->d_top_pos,
-                                                               g[cur], (int)p->WL, p->R, B, ld);
+    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, g[cur], (int)p->WL, p->R, B, ld, s);
+    ++g_launches;
   }
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
-    BwdArgs<T> a;
+    LayerArgs<T> a = layer_args<T>(p, d, false, V, ld);
+    a.out = g[cur ^ 1];
     a.gcur = g[cur];
-    a.gprev = g[cur ^ 1];
     a.ncur = trace + (size_t)d.row * ld;
     a.nprev = trace + (size_t)d.prev_row * ld;
-    a.toff = p->d_toff + d.toff_base;
-    a.tpar = p->d_tpar + d.e_base;
-    a.off = p->d_off + d.off_base;
-    a.src = p->d_src + d.e_base;
-    a.Wprev = (int)d.Wprev;
-    a.V = V;
-    a.ld = ld;
-    Launch L = row_launch(d.Wprev, V);
+    a.scratch = scratch;
+    int mode = BW_PASS_;
+    if (domain == SR_REAL_ && d.prod) mode = BW_REALPROD_;
+    else if (domain == SR_LOG_ && !d.prod) mode = BW_LOGSUM_;
     LaunchScope ls(s, 1, l + 1);
-    if (domain == SR_REAL && d.prod)
-      bwd_layer_kernel<T, BW_REALPROD><<<L.grid, L.block, 0, s>>>(a);
-    else if (domain == SR_LOG && !d.prod)
-      bwd_layer_kernel<T, BW_LOGSUM><<<L.grid, L.block, 0, s>>>(a);
-    else
-      bwd_layer_kernel<T, BW_PASS><<<L.grid, L.block, 0, s>>>(a);
+    g_launches += launch_backward_layer(mode, a, s);
     cur ^= 1;
   }
-  if (p->K > 0 && B > 0) {
-    dim3 grid((unsigned)((B + 31) / 32), (unsigned)((p->K + 31) / 32));
+  if (p->K > 0) {
     LaunchScope ls(s, 3, 0);
-    store_rows_kernel<T><<<grid, dim3(32, 8), 0, s>>>(g[cur], grads, (int)p->K, B, ld);
+    launch_store_rows<T>(g[cur], grads, (int)p->K, B, ld, s);
+    ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());
+  return KLAY_OK;
+}
+
+int check_common(const KlayPlan* plan, int32_t dtype, int64_t batch, int64_t ld) {
+  if (!plan) return fail(KLAY_EINVAL, "plan is NULL");
+  if (dtype != KLAY_F32 && dtype != KLAY_F64) return fail(KLAY_EINVAL, "unknown dtype");
+  if (batch < 1) return fail(KLAY_EINVAL, "batch must be >= 1");
+  if (ld < klay_row_stride(batch, dtype) || (ld * (int64_t)esize(dtype)) % 16)
+    return fail(KLAY_EINVAL, "row stride too small or not a multiple of 16 bytes");
   return KLAY_OK;
 }
 
@@ -395,42 +472,33 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
 extern "C" int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
                             const void* weights, int32_t weights_dtype, void* values, int64_t ld,
                             int32_t retain, void* outputs, int64_t batch, double epsilon,
-                            void* stream) {
-  if (!plan) return fail(KLAY_EINVAL, "plan is NULL");
+                            void* workspace, void* stream) {
+  if (int rc = check_common(plan, dtype, batch, ld)) return rc;
   if (semiring < KLAY_REAL || semiring > KLAY_MAXPROD) return fail(KLAY_EINVAL, "unknown semiring");
-  if (dtype != KLAY_F32 && dtype != KLAY_F64) return fail(KLAY_EINVAL, "unknown dtype");
   if (weights_dtype != KLAY_F32 && weights_dtype != KLAY_F64) return fail(KLAY_EINVAL, "unknown weights dtype");
-  if (batch < 1) return fail(KLAY_EINVAL, "batch must be >= 1");
-  if (ld < klay_row_stride(batch, dtype) || (ld * (dtype == KLAY_F64 ? 8 : 4)) % 16)
-    return fail(KLAY_EINVAL, "row stride too small or not a multiple of 16 bytes");
   if (semiring == KLAY_LOG && !(epsilon >= 0)) return fail(KLAY_EINVAL, "epsilon must be >= 0");
   if (!values || (plan->K > 0 && !weights)) return fail(KLAY_EINVAL, "NULL buffer");
-  if ((reinterpret_cast<uintptr_t>(values) & 15) != 0) return fail(KLAY_EINVAL, "values not 16-byte aligned");
+  if (plan->max_fslots > 0 && !workspace) return fail(KLAY_EINVAL, "workspace required (klay_forward_workspace)");
+  if ((reinterpret_cast<uintptr_t>(values) & 15) != 0 || (reinterpret_cast<uintptr_t>(workspace) & 15) != 0)
+    return fail(KLAY_EINVAL, "buffers must be 16-byte aligned");
   DeviceGuard guard(plan->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == KLAY_F32)
     return forward_impl<float>(plan, semiring, weights, weights_dtype, (float*)values, ld, retain != 0,
-                               (float*)outputs, batch, epsilon, s);
+                               (float*)outputs, batch, epsilon, (float*)workspace, s);
   return forward_impl<double>(plan, semiring, weights, weights_dtype, (double*)values, ld, retain != 0,
-                              (double*)outputs, batch, epsilon, s);
-}
-
-extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
-  if (!plan) return 0;
-  return (size_t)2 * plan->max_width * ld * (dtype == KLAY_F64 ? 8 : 4);
+                              (double*)outputs, batch, epsilon, (double*)workspace, s);
 }
 
 extern "C" int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                              int64_t ld, const void* seed, void* grads, void* workspace, int64_t batch,
                              void* stream) {
-  if (!plan) return fail(KLAY_EINVAL, "plan is NULL");
+  if (int rc = check_common(plan, dtype, batch, ld)) return rc;
   if (domain != KLAY_REAL && domain != KLAY_LOG)
     return fail(KLAY_EUNSUPPORTED, "backward is defined for the real and log domains only");
-  if (dtype != KLAY_F32 && dtype != KLAY_F64) return fail(KLAY_EINVAL, "unknown dtype");
-  if (batch < 1) return fail(KLAY_EINVAL, "batch must be >= 1");
-  if (ld < klay_row_stride(batch, dtype) || (ld * (dtype == KLAY_F64 ? 8 : 4)) % 16)
-    return fail(KLAY_EINVAL, "row stride too small or not a multiple of 16 bytes");
   if (!trace || !workspace || (plan->K > 0 && !grads)) return fail(KLAY_EINVAL, "NULL buffer");
+  if ((reinterpret_cast<uintptr_t>(trace) & 15) != 0 || (reinterpret_cast<uintptr_t>(workspace) & 15) != 0)
+    return fail(KLAY_EINVAL, "buffers must be 16-byte aligned");
   DeviceGuard guard(plan->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == KLAY_F32)

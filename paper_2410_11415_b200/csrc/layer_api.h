@@ -1,0 +1,54 @@
+// Host-visible interface between the C-ABI layer (klay.cu) and the kernel
+// translation units (fwd_*.cu, bwd_*.cu, boundary.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace klay {
+
+template <typename T>
+struct LayerArgs {
+  const int4* items;  // work items of this layer/direction
+  int n_items;
+  const int4* heavy;  // {node, first leaf slot, #leaves, 0}
+  int n_heavy;
+  const int* off;     // segment offsets [nodes+1]
+  const int* idx;     // edge -> operand row
+  T* out;             // output rows
+  T* scratch;         // leaf partials [slots, ld] (+ [slots, ld] t-part for LSE)
+  long long tpart;    // element offset of the LSE t-part inside scratch
+  int V;              // 16-byte vectors per row
+  long long ld;
+  T eps;
+  // forward operand
+  const T* prev;
+  // backward operands
+  const T* gcur;      // adjoint rows of the layer above (parents)
+  const T* ncur;      // forward values of the parents
+  const T* nprev;     // forward values of the children (own value x)
+  const int* foff;    // forward CSR (real-product zero path)
+  const int* fsrc;
+};
+
+// forward layer: semiring x layer op -> reduction kind (RK_*)
+int launch_forward_layer(int sr, bool prod, const LayerArgs<float>& a, cudaStream_t s);
+int launch_forward_layer(int sr, bool prod, const LayerArgs<double>& a, cudaStream_t s);
+// backward layer (BW_* mode): always a pairwise sum over each child's out-edges
+int launch_backward_layer(int mode, const LayerArgs<float>& a, cudaStream_t s);
+int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s);
+
+// boundary kernels
+template <typename T>
+void launch_load_inputs(const void* w, bool w_f64, T* n0, int K, long long B, long long ld, T pad,
+                        cudaStream_t s);
+template <typename T>
+void launch_store_rows(const T* rows, T* out, int Q, long long B, long long ld, cudaStream_t s);
+template <typename T>
+void launch_assemble_outputs(const T* last, const int* root_node, const signed char* const_val,
+                             T* out, int R, long long B, long long ld, T zero, T one,
+                             cudaStream_t s);
+template <typename T>
+void launch_seed(const T* seed, const int* top_off, const int* top_pos, T* g, int WL, int R,
+                 long long B, long long ld, cudaStream_t s);
+
+}  // namespace klay

@@ -241,8 +241,17 @@ class DevicePlan:
         tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
         return torch.empty((rows, ld), dtype=tdt, device=self.device)
 
+    def forward_workspace(self, batch: int, dtype):
+        """Scratch for split (heavy) segments, or None when not needed."""
+        torch = _torch()
+        ld = self.row_stride(batch, dtype)
+        nbytes = int(self._lib.klay_forward_workspace(self._handle, _klay_dtype(dtype), ld))
+        if nbytes == 0:
+            return None
+        return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
     def forward(self, weights, semiring: int, dtype, retain=True, epsilon=0.0,
-                values=None, outputs=None):
+                values=None, outputs=None, workspace=None):
         """weights: cuda tensor [B, K] (float32/float64, semiring domain).
         Returns (outputs [B, R] tensor, values buffer [rows, ld])."""
         torch = _torch()
@@ -262,10 +271,13 @@ class DevicePlan:
         tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
         if outputs is None:
             outputs = torch.empty((B, self.num_roots), dtype=tdt, device=self.device)
+        if workspace is None:
+            workspace = self.forward_workspace(B, dtype)
         rc = self._lib.klay_forward(
             self._handle, semiring, _klay_dtype(dtype), weights.data_ptr(), wdt,
             values.data_ptr(), ld, 1 if retain else 0,
-            outputs.data_ptr() if self.num_roots else None, B, float(epsilon), self._stream())
+            outputs.data_ptr() if self.num_roots else None, B, float(epsilon),
+            workspace.data_ptr() if workspace is not None else None, self._stream())
         _lib.check(rc, "klay_forward")
         return outputs, values
 

@@ -58,7 +58,7 @@ def test_row_stride_and_plan_errors_without_gpu():
                               ctypes.byref(h))
     assert rc == _lib.KLAY_EFORMAT
     assert "out of range" in _lib.last_error()
-    assert lib.klay_forward(None, 0, 0, None, 0, None, 4, 1, None, 1, 0.0, None) == _lib.KLAY_EINVAL
+    assert lib.klay_forward(None, 0, 0, None, 0, None, 4, 1, None, 1, 0.0, None, None) == _lib.KLAY_EINVAL
 
 
 @pytest.mark.parametrize("name", SMALL_CASES)
