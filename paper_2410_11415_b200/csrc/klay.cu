@@ -88,7 +88,9 @@ void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
 }
 
 // Balanced work items over one CSR (W segments, offsets off[base..base+W]).
-void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s) {
+// split == false keeps every segment in one item (sequential reductions:
+// np.multiply.reduceat has no exact parallel decomposition).
+void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s, bool split = true) {
   std::vector<int4> leaves, singles, ranges;
   std::vector<std::pair<int, int>> lv;
   int rb = -1, re_edges = 0;
@@ -100,7 +102,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s) {
   };
   for (int p = 0; p < W; ++p) {
     const int s0 = off[base + p], n = off[base + p + 1] - s0;
-    if (n - 1 > PW_BLOCK_H) {
+    if (split && n - 1 > PW_BLOCK_H) {
       flush(p);
       lv.clear();
       split_leaves(s0 + 1, n - 1, lv);
@@ -130,6 +132,7 @@ struct LayerDesc {
   int64_t e_base;         // into src[] / tpar[]
   int64_t toff_base;      // into toff[] (Wprev+1 entries per layer)
   int64_t fi_base, fi_n, fh_base, fh_n, f_slots;  // forward items / heavy
+  int64_t fq_base, fq_n;                           // forward items, no split (PROD)
   int64_t bi_base, bi_n, bh_base, bh_n, b_slots;  // backward items / heavy
 };
 
@@ -281,6 +284,15 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
+    d.fq_base = d.fi_base;
+    d.fq_n = d.fi_n;
+    if (d.prod && !fs.heavy.empty()) {
+      ItemSet qs;
+      build_items(off, (size_t)d.off_base, (int)W, qs, false);
+      d.fq_base = (int64_t)items.size();
+      d.fq_n = (int64_t)qs.items.size();
+      items.insert(items.end(), qs.items.begin(), qs.items.end());
+    }
     d.bi_base = (int64_t)items.size();
     d.bi_n = (int64_t)bs.items.size();
     items.insert(items.end(), bs.items.begin(), bs.items.end());
@@ -402,6 +414,12 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
     LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
+    if (d.prod && (sr == SR_REAL_ || sr == KLAY_MAXPROD)) {
+      // sequential product: heavy segments stay whole (no leaves, no combine)
+      a.items = p->d_items + d.fq_base;
+      a.n_items = (int)d.fq_n;
+      a.n_heavy = 0;
+    }
     a.out = cur;
     a.prev = prev;
     a.eps = (T)eps;
