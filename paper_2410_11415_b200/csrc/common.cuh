@@ -174,33 +174,52 @@ template <typename T>
 struct LseOp {
   Vec<T> m, t;
   T eps;
+  int k;
   __device__ __forceinline__ void begin(int) {
     m = vfill<T>(T(-INFINITY));
     t = vfill<T>(T(0));
+    k = 0;
   }
   __device__ __forceinline__ void begin_leaf(int n) { begin(n); }
   __device__ __forceinline__ void push(const Vec<T>& x) {
 #pragma unroll
     for (int c = 0; c < Vec<T>::N; ++c) {
       const T xv = x.v[c];
-      if (xv > m.v[c]) {
+      if (k == 0) {
+        // first element: exp(x - x) = 1, or 0 for an all -inf prefix (NaN -> 0)
+        m.v[c] = xv;
+        t.v[c] = (xv == T(-INFINITY)) ? T(0) : T(1);
+      } else if (xv > m.v[c]) {
         t.v[c] = t.v[c] * kexp(m.v[c] - xv) + T(1);
         m.v[c] = xv;
       } else if (xv != T(-INFINITY)) {
         t.v[c] = t.v[c] + kexp(xv - m.v[c]);
       }
     }
+    ++k;
   }
   __device__ __forceinline__ Vec<T> result() const {
     Vec<T> r;
 #pragma unroll
     for (int c = 0; c < Vec<T>::N; ++c) {
-      const T res = klog(t.v[c] + eps) + m.v[c];
+      // log(1 + 0) + m == m exactly: unary segments (79% of sum nodes) skip the log
+      const T res = (t.v[c] == T(1) && eps == T(0)) ? m.v[c] : klog(t.v[c] + eps) + m.v[c];
       r.v[c] = (m.v[c] == T(-INFINITY)) ? T(-INFINITY) : res;
     }
     return r;
   }
 };
+
+// ---- cp.async (LDGSTS) helpers: 16-byte global -> shared copies ------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // pairwise-tree combination of leaf partials stored one row apart
 // (same recursion as numpy's pairwise_sum above PW_BLOCK elements)

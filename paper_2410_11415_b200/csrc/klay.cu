@@ -90,7 +90,11 @@ void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
 // Balanced work items over one CSR (W segments, offsets off[base..base+W]).
 // split == false keeps every segment in one item (sequential reductions:
 // np.multiply.reduceat has no exact parallel decomposition).
+// Range items hold <= cap edges: cap shrinks for narrow layers so that even
+// thin layers spread over many warps (short per-warp dependency chains).
 void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s, bool split = true) {
+  const int E = off[base + W] - off[base];
+  const int cap = std::max(8, std::min(ITEM_EDGES, (E / 296) & ~7));
   std::vector<int4> leaves, singles, ranges;
   std::vector<std::pair<int, int>> lv;
   int rb = -1, re_edges = 0;
@@ -108,11 +112,11 @@ void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s, bo
       split_leaves(s0 + 1, n - 1, lv);
       s.heavy.push_back(make_int4(p, s.slots, (int)lv.size(), 0));
       for (auto& l : lv) leaves.push_back(make_int4(p, -(s.slots++) - 1, l.first, l.second));
-    } else if (n > ITEM_EDGES) {
+    } else if (n > cap) {
       flush(p);
       singles.push_back(make_int4(p, p + 1, s0, s0 + n));
     } else {
-      if (rb >= 0 && (p - rb >= ITEM_NODES || re_edges + n > ITEM_EDGES)) flush(p);
+      if (rb >= 0 && (p - rb >= ITEM_NODES || re_edges + n > cap)) flush(p);
       if (rb < 0) rb = p;
       re_edges += n;
     }

@@ -23,87 +23,104 @@ constexpr int WARPS_PER_BLOCK = 4;
 
 
 // ---- operand policies -------------------------------------------------------
+// issue():  cp.async this lane's 16 bytes of every operand row of one edge
+//           into the edge's staging slot (NOP operand vectors per lane)
+// value():  the edge's contribution, from the staged operands
+// NX:       a per-node own value is staged too (backward: the child's x)
 
 template <typename T>
 struct FwdGather {
-  struct Opnd { Vec<T> a; };
-  static constexpr int EB = 16;
+  static constexpr int NOP = 1, NX = 0, EB = 8;
   const T* base;
   long long ld;
   __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col) : base(a.prev + col), ld(a.ld) {}
-  __device__ __forceinline__ void node_begin(int, bool) {}
-  __device__ __forceinline__ Opnd load(int row) const { return {ldv(base + (size_t)row * ld)}; }
-  __device__ __forceinline__ Vec<T> value(const Opnd& o, int) const { return o.a; }
+  __device__ __forceinline__ void issue(Vec<T>* slot, int row, int lane) const {
+    cp_async16(slot + lane, base + (size_t)row * ld);
+  }
+  __device__ __forceinline__ void issue_x(Vec<T>*, int, int) const {}
+  __device__ __forceinline__ Vec<T> value(const Vec<T>* slot, int lane, int, const Vec<T>&) const {
+    return slot[lane];
+  }
+  __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>&) const {
+    return ldv(base + (size_t)row * ld);
+  }
+  __device__ __forceinline__ Vec<T> load_x(int) const { return Vec<T>{}; }
 };
 
 template <typename T, int MODE>
 struct BwdGather {
-  struct Opnd { Vec<T> g, P; };
-  static constexpr int EB = (MODE == BW_PASS) ? 16 : 8;
+  static constexpr int NOP = (MODE == BW_PASS) ? 1 : 2;
+  static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
+  static constexpr int EB = (MODE == BW_PASS) ? 8 : 4;
   const T* gbase;
   const T* nbase;
   const T* xbase;
-  const T* pbase;
   const int* foff;
   const int* fsrc;
   long long ld;
-  Vec<T> x;
   __device__ __forceinline__ BwdGather(const LayerArgs<T>& a, size_t col)
-      : gbase(a.gcur + col), nbase(a.ncur + col), xbase(a.nprev + col), pbase(a.nprev + col),
-        foff(a.foff), fsrc(a.fsrc), ld(a.ld) {}
-  __device__ __forceinline__ void node_begin(int node, bool active) {
-    if (MODE != BW_PASS && active) x = ldv(xbase + (size_t)node * ld);
+      : gbase(a.gcur + col), nbase(a.ncur + col), xbase(a.nprev + col), foff(a.foff),
+        fsrc(a.fsrc), ld(a.ld) {}
+  __device__ __forceinline__ void issue(Vec<T>* slot, int row, int lane) const {
+    cp_async16(slot + lane, gbase + (size_t)row * ld);
+    if constexpr (NOP == 2) cp_async16(slot + 32 + lane, nbase + (size_t)row * ld);
   }
-  __device__ __forceinline__ Opnd load(int row) const {
-    Opnd o;
-    o.g = ldv(gbase + (size_t)row * ld);
-    if (MODE != BW_PASS) o.P = ldv(nbase + (size_t)row * ld);
-    return o;
+  __device__ __forceinline__ void issue_x(Vec<T>* slot, int node, int lane) const {
+    cp_async16(slot + lane, xbase + (size_t)node * ld);
   }
-  __device__ __forceinline__ Vec<T> value(const Opnd& o, int row) const {
+  __device__ __forceinline__ Vec<T> load_x(int node) const { return ldv(xbase + (size_t)node * ld); }
+  __device__ __forceinline__ Vec<T> value(const Vec<T>* slot, int lane, int row, const Vec<T>& x) const {
+    if constexpr (NOP == 2) return combine(slot[lane], slot[32 + lane], row, x);
+    else return slot[lane];
+  }
+  __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>& x) const {
+    const Vec<T> g = ldv(gbase + (size_t)row * ld);
+    if constexpr (NOP == 2) return combine(g, ldv(nbase + (size_t)row * ld), row, x);
+    else return g;
+  }
+  __device__ __forceinline__ Vec<T> combine(const Vec<T>& g, const Vec<T>& P, int row,
+                                            const Vec<T>& x) const {
     constexpr int N = Vec<T>::N;
-    if constexpr (MODE == BW_PASS) {
-      // log-domain products / real-domain sums: parent adjoint passes through
-      return o.g;
-    } else if constexpr (MODE == BW_LOGSUM) {
+    Vec<T> r;
+    if constexpr (MODE == BW_LOGSUM) {
       // g[parent] * exp(child - parent); NaN/inf weights -> 0 (engine.py:346-352)
-      Vec<T> r;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        T w = kexp(x.v[c] - o.P.v[c]);
+        T w = kexp(x.v[c] - P.v[c]);
         w = isfinite(w) ? w : T(0);
-        r.v[c] = o.g.v[c] * w;
+        r.v[c] = g.v[c] * w;
       }
-      return r;
     } else {
-      // zero-safe product adjoint (engine.py:358-369)
-      Vec<T> r;
+      // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
+      // child gets g * (product of nonzero siblings) iff it is the only zero
       bool any_zero = false;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        r.v[c] = (o.g.v[c] * o.P.v[c]) / x.v[c];
+        r.v[c] = (g.v[c] * P.v[c]) / x.v[c];
         any_zero |= (x.v[c] == T(0));
       }
-      if (any_zero) {
-        const int s0 = __ldg(foff + row), s1 = __ldg(foff + row + 1);
-        T pnz[N];
-        int zc[N];
-#pragma unroll
-        for (int c = 0; c < N; ++c) { pnz[c] = T(1); zc[c] = 0; }
-        for (int s = s0; s < s1; ++s) {
-          Vec<T> y = ldv(pbase + (size_t)__ldg(fsrc + s) * ld);
-#pragma unroll
-          for (int c = 0; c < N; ++c) {
-            if (y.v[c] == T(0)) ++zc[c];
-            else pnz[c] *= y.v[c];
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < N; ++c)
-          if (x.v[c] == T(0)) r.v[c] = (zc[c] == 1) ? o.g.v[c] * pnz[c] : T(0);
-      }
-      return r;
+      if (any_zero) zero_path(r, g, row, x);
     }
+    return r;
+  }
+  __device__ __noinline__ void zero_path(Vec<T>& r, const Vec<T>& g, int row, const Vec<T>& x) const {
+    constexpr int N = Vec<T>::N;
+    const int s0 = __ldg(foff + row), s1 = __ldg(foff + row + 1);
+    T pnz[N];
+    int zc[N];
+#pragma unroll
+    for (int c = 0; c < N; ++c) { pnz[c] = T(1); zc[c] = 0; }
+    for (int s = s0; s < s1; ++s) {
+      const Vec<T> y = ldv(xbase + (size_t)__ldg(fsrc + s) * ld);
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        if (y.v[c] == T(0)) ++zc[c];
+        else pnz[c] *= y.v[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+      if (x.v[c] == T(0)) r.v[c] = (zc[c] == 1) ? g.v[c] * pnz[c] : T(0);
   }
 };
 
@@ -116,61 +133,112 @@ struct OpFor<T, RK_SUM> { using type = SumOp<T>; };
 template <typename T>
 struct OpFor<T, RK_LSE> { using type = LseOp<T>; };
 
+constexpr int ITEM_IDX = 128;  // edge indices staged per item (longer items read idx directly)
+
 template <typename T, int RK, typename G>
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, 4) items_kernel(LayerArgs<T> a) {
+struct ItemsSmem {
+  static constexpr int SLOT = (G::NOP + G::NX) * 32;  // Vec<T> per edge slot
+  static constexpr size_t stage = (size_t)WARPS_PER_BLOCK * 2 * G::EB * SLOT * sizeof(Vec<T>);
+  static constexpr size_t accum = (RK == RK_SUM) ? (size_t)8 * WARPS_PER_BLOCK * 32 * sizeof(Vec<T>) : 0;
+  static constexpr size_t index = (size_t)WARPS_PER_BLOCK * (ITEM_IDX + 32) * sizeof(int);
+  static constexpr size_t bytes = stage + accum + index;
+};
+
+template <typename T, int RK, typename G>
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T> a) {
   using Op = typename OpFor<T, RK>::type;
-  constexpr int EB = G::EB;
+  using S = ItemsSmem<T, RK, G>;
+  constexpr int EB = G::EB, SLOT = S::SLOT;
+  extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
-  if (item >= a.n_items) return;
+  if (item >= a.n_items) return;  // no block-wide barriers below
+  Vec<T>* stage = reinterpret_cast<Vec<T>*>(smem) + (size_t)warp * 2 * EB * SLOT;
+  int* widx = reinterpret_cast<int*>(smem + S::stage + S::accum) + warp * (ITEM_IDX + 32);
+  int* wend = widx + ITEM_IDX;
+
   const int v = blockIdx.y * 32 + lane;
   const bool active = v < a.V;
   const size_t col = (size_t)v * Vec<T>::N;
   const long long ld = a.ld;
   const int4 it = __ldg(a.items + item);
-  G g(a, col);
+  const bool leaf = it.y < 0;
+  const int nn = leaf ? 1 : it.y - it.x;
+  const int ne = it.w - it.z;
+  const bool staged_idx = ne <= ITEM_IDX;
+  const G g(a, col);
   Op op;
   if constexpr (RK == RK_LSE) op.eps = a.eps;
   if constexpr (RK == RK_SUM) {
-    __shared__ Vec<T> accum[8][WARPS_PER_BLOCK * 32];
-    op.r = &accum[0][threadIdx.x];
+    op.r = reinterpret_cast<Vec<T>*>(smem + S::stage) + threadIdx.x;
     op.rstride = WARPS_PER_BLOCK * 32;
   }
+  // the item's edge indices and (relative) segment ends, one round trip
+  if (staged_idx)
+    for (int q = lane; q < ne; q += 32) widx[q] = __ldg(a.idx + it.z + q);
+  if (!leaf && lane < nn) wend[lane] = __ldg(a.off + it.x + 1 + lane) - it.z;
+  __syncwarp();
 
-  const bool leaf = it.y < 0;
-  const int nn = leaf ? 1 : it.y - it.x;
-  int my_end = 0;
-  if (!leaf && lane < nn) my_end = __ldg(a.off + it.x + 1 + lane);
-  int node = 0;
-  int seg_end = leaf ? it.w : __shfl_sync(0xffffffffu, my_end, 0);
-  g.node_begin(it.x, active);
-  if (leaf) op.begin_leaf(it.w - it.z);
-  else op.begin(seg_end - it.z);
-
-  for (int e = it.z; e < it.w; e += EB) {
-    const int cnt = min(EB, it.w - e);
-    const int my_idx = (lane < cnt) ? __ldg(a.idx + e + lane) : 0;
-    typename G::Opnd o[EB];
-    int rows[EB];
-#pragma unroll
-    for (int i = 0; i < EB; ++i) {
-      rows[i] = __shfl_sync(0xffffffffu, my_idx, i);
-      if (i < cnt && active) o[i] = g.load(rows[i]);
+  // stage batch b: operand rows of edges [b*EB, b*EB+cnt) and the own value
+  // of every node whose segment starts in the batch
+  int xnode = 0, xstart = 0;
+  auto issue = [&](int b) {
+    const int base = b * EB;
+    const int cnt = min(EB, ne - base);
+    Vec<T>* st = stage + (b & 1) * EB * SLOT;
+    if (active) {
+      for (int i = 0; i < cnt; ++i) {
+        const int row = staged_idx ? widx[base + i] : __ldg(a.idx + it.z + base + i);
+        g.issue(st + i * SLOT, row, lane);
+      }
     }
-#pragma unroll
-    for (int i = 0; i < EB; ++i) {
-      if (i < cnt) {
-        if (active) op.push(g.value(o[i], rows[i]));
-        else op.push(vfill<T>(T(0)));
-        if (!leaf && e + i + 1 == seg_end) {
-          if (active) stv(a.out + (size_t)(it.x + node) * ld + col, op.result());
-          ++node;
-          if (node < nn) {
-            const int seg_start = seg_end;
-            seg_end = __shfl_sync(0xffffffffu, my_end, node);
-            g.node_begin(it.x + node, active);
-            op.begin(seg_end - seg_start);
-          }
+    if constexpr (G::NX) {
+      if (leaf) {
+        if (b == 0 && active) g.issue_x(st + G::NOP * 32, it.x, lane);
+      } else {
+        while (xnode < nn && xstart < base + cnt) {
+          if (active) g.issue_x(st + (xstart - base) * SLOT + G::NOP * 32, it.x + xnode, lane);
+          xstart = wend[xnode];
+          ++xnode;
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int nb = (ne + EB - 1) / EB;
+  int node = 0, seg_start = 0;
+  int seg_end = leaf ? ne : wend[0];
+  if (leaf) op.begin_leaf(ne);
+  else op.begin(seg_end);
+  Vec<T> x{};
+  issue(0);
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb) {
+      issue(b + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    const Vec<T>* st = stage + (b & 1) * EB * SLOT;
+    const int base = b * EB;
+    const int cnt = min(EB, ne - base);
+    for (int i = 0; i < cnt; ++i) {
+      const int k = base + i;
+      if constexpr (G::NX) {
+        if (k == seg_start && (!leaf || k == 0)) x = st[i * SLOT + G::NOP * 32 + lane];
+      }
+      if (active) {
+        const int row = (G::NX && G::NOP == 2) ? (staged_idx ? widx[k] : __ldg(a.idx + it.z + k)) : 0;
+        op.push(g.value(st + i * SLOT, lane, row, x));
+      }
+      if (!leaf && k + 1 == seg_end) {
+        if (active) stv(a.out + (size_t)(it.x + node) * ld + col, op.result());
+        ++node;
+        if (node < nn) {
+          seg_start = seg_end;
+          seg_end = wend[node];
+          op.begin(seg_end - seg_start);
         }
       }
     }
@@ -199,10 +267,9 @@ __global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
   const int node = hv.x, slot0 = hv.y, nl = hv.z;
   const int s = __ldg(a.off + node);
   const int n = __ldg(a.off + node + 1) - s;
-  G g(a, col);
-  g.node_begin(node, true);
-  const int row0 = __ldg(a.idx + s);
-  const Vec<T> x0 = g.value(g.load(row0), row0);
+  const G g(a, col);
+  const Vec<T> x = g.load_x(node);
+  const Vec<T> x0 = g.direct(__ldg(a.idx + s), x);
   Vec<T> res;
   if constexpr (RK == RK_SUM) {
     int leaf = slot0;
@@ -235,8 +302,15 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
   int launched = 0;
   if (a.n_items > 0) {
     ++launched;
+    constexpr size_t smem = ItemsSmem<T, RK, G>::bytes;
+    static bool configured = false;  // opt in to > 48 KB dynamic smem once per kernel
+    if (!configured) {
+      cudaFuncSetAttribute(items_kernel<T, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      configured = true;
+    }
     dim3 grid((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
-    items_kernel<T, RK, G><<<grid, WARPS_PER_BLOCK * 32, 0, s>>>(a);
+    items_kernel<T, RK, G><<<grid, WARPS_PER_BLOCK * 32, smem, s>>>(a);
   }
   if (a.n_heavy > 0) {
     ++launched;
