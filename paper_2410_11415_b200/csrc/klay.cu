@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -22,9 +23,11 @@ enum { SR_REAL_ = 0, SR_LOG_ = 1 };
 enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2 };
 
 // work-item shape (see layer_kernels.cuh)
-constexpr int ITEM_EDGES = 64;   // edges per range item
-constexpr int ITEM_NODES = 31;   // nodes per range item (one lane per segment end)
-constexpr int PW_BLOCK_H = 128;  // numpy pairwise block; longer tails are split
+constexpr int TASK_EDGES_H = 128;  // edges per short task (== TASK_EDGES)
+constexpr int TASK_NODES_H = 128;  // nodes per short task (== TASK_NODES)
+constexpr int SHORT_FWD = 16;      // FwdGather::SE
+constexpr int SHORT_BWD = 8;       // BwdGather::SE
+constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are split
 
 thread_local std::string g_err;
 
@@ -51,6 +54,12 @@ struct ProfRec {
 thread_local bool g_prof_on = false;
 thread_local std::vector<ProfRec> g_prof;
 
+// KLAY_SYNC_DEBUG=1: synchronize after every launch and report the failing one
+const bool g_sync_debug = [] {
+  const char* e = getenv("KLAY_SYNC_DEBUG");
+  return e && *e && *e != '0';
+}();
+
 struct LaunchScope {
   cudaStream_t s;
   int kind, layer;
@@ -66,6 +75,11 @@ struct LaunchScope {
     if (g_prof_on) {
       cudaEventRecord(b, s);
       g_prof.push_back({kind, layer, a, b});
+    }
+    if (g_sync_debug) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) fprintf(stderr, "libklay: launch kind %d layer %d failed: %s\n", kind, layer,
+                                    cudaGetErrorString(e));
     }
   }
 };
@@ -87,22 +101,27 @@ void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
   split_leaves(a + n2, len - n2, out);
 }
 
-// Balanced work items over one CSR (W segments, offsets off[base..base+W]).
-// split == false keeps every segment in one item (sequential reductions:
-// np.multiply.reduceat has no exact parallel decomposition).
-// Range items hold <= cap edges: cap shrinks for narrow layers so that even
-// thin layers spread over many warps (short per-warp dependency chains).
-void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s, bool split = true) {
+// Work items over one CSR (W segments, offsets off[base..base+W]); kinds as
+// documented at items_kernel (layer_kernels.cuh):
+//   segments with <= short_max edges are packed into short tasks of <= cap
+//   edges and <= TASK_NODES_H nodes; longer ones become long items; with
+//   split, tails longer than one numpy pairwise block become leaf items.
+// split == false keeps every segment whole (np.multiply.reduceat is
+// sequential: it has no exact parallel decomposition).
+// cap shrinks for narrow layers so that thin layers still spread over many
+// warps (short per-warp dependency chains).
+void build_items(const std::vector<int>& off, size_t base, int W, int short_max, ItemSet& s,
+                 bool split = true) {
   const int E = off[base + W] - off[base];
-  const int cap = std::max(8, std::min(ITEM_EDGES, (E / 296) & ~7));
-  std::vector<int4> leaves, singles, ranges;
+  const int cap = std::max(short_max, std::min(TASK_EDGES_H, (E / 296) & ~7));
+  std::vector<int4> leaves, longs, shorts;
   std::vector<std::pair<int, int>> lv;
-  int rb = -1, re_edges = 0;
+  int tb = -1, t_edges = 0;
   auto flush = [&](int end_node) {
-    if (rb >= 0 && end_node > rb)
-      ranges.push_back(make_int4(rb, end_node, off[base + rb], off[base + end_node]));
-    rb = -1;
-    re_edges = 0;
+    if (tb >= 0 && end_node > tb)
+      shorts.push_back(make_int4(tb, end_node, off[base + tb], off[base + end_node]));
+    tb = -1;
+    t_edges = 0;
   };
   for (int p = 0; p < W; ++p) {
     const int s0 = off[base + p], n = off[base + p + 1] - s0;
@@ -112,20 +131,20 @@ void build_items(const std::vector<int>& off, size_t base, int W, ItemSet& s, bo
       split_leaves(s0 + 1, n - 1, lv);
       s.heavy.push_back(make_int4(p, s.slots, (int)lv.size(), 0));
       for (auto& l : lv) leaves.push_back(make_int4(p, -(s.slots++) - 1, l.first, l.second));
-    } else if (n > cap) {
+    } else if (n > short_max) {
       flush(p);
-      singles.push_back(make_int4(p, p + 1, s0, s0 + n));
+      longs.push_back(make_int4(p, 0, s0, s0 + n));
     } else {
-      if (rb >= 0 && (p - rb >= ITEM_NODES || re_edges + n > cap)) flush(p);
-      if (rb < 0) rb = p;
-      re_edges += n;
+      if (tb >= 0 && (p - tb >= TASK_NODES_H || t_edges + n > cap)) flush(p);
+      if (tb < 0) tb = p;
+      t_edges += n;
     }
   }
   flush(W);
-  s.items.reserve(leaves.size() + singles.size() + ranges.size());
+  s.items.reserve(leaves.size() + longs.size() + shorts.size());
   s.items.insert(s.items.end(), leaves.begin(), leaves.end());
-  s.items.insert(s.items.end(), singles.begin(), singles.end());
-  s.items.insert(s.items.end(), ranges.begin(), ranges.end());
+  s.items.insert(s.items.end(), longs.begin(), longs.end());
+  s.items.insert(s.items.end(), shorts.begin(), shorts.end());
 }
 
 struct LayerDesc {
@@ -283,8 +302,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     for (int64_t e = 0; e < E; ++e) tpar[tb + pos[S[e]]++] = (int)G[e];
     // work items: forward over parents, backward over children
     ItemSet fs, bs;
-    build_items(off, (size_t)d.off_base, (int)W, fs);
-    build_items(toff, (size_t)d.toff_base, (int)prev_w, bs);
+    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs);
+    build_items(toff, (size_t)d.toff_base, (int)prev_w, SHORT_BWD, bs);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
@@ -292,7 +311,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.fq_n = d.fi_n;
     if (d.prod && !fs.heavy.empty()) {
       ItemSet qs;
-      build_items(off, (size_t)d.off_base, (int)W, qs, false);
+      build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, qs, false);
       d.fq_base = (int64_t)items.size();
       d.fq_n = (int64_t)qs.items.size();
       items.insert(items.end(), qs.items.begin(), qs.items.end());

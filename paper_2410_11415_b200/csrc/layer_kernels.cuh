@@ -1,17 +1,12 @@
 // Layer kernels of libklay: one warp per (work item, 512-byte column chunk).
 //
 // Work items are built on the host per layer and direction (klay.cu,
-// build_items): a *range item* covers consecutive whole segments (<= 31
-// nodes, <= ITEM_EDGES edges, or one larger node); a *leaf item* covers one
-// numpy-pairwise leaf (<= 128 edges) of a heavy segment (fan-in > 129),
-// whose partial goes to scratch and is combined in pairwise-tree order by
-// the combine kernel. The warp streams its item's edges in batches of EB:
-// lane i fetches edge i's row index (one coalesced load), the indices are
-// broadcast with shuffles and every lane issues EB independent 128-bit row
-// loads (its 16 bytes of each child row chunk) before reducing them in edge
-// order. Column chunks are the slow grid dimension, so all items of chunk 0
-// run before chunk 1: the previous layer's working set per chunk is
-// W_prev x 512 B (35 MB at the widest layer of config C), L2-resident.
+// build_items; kinds documented at items_kernel). Heavy segments (fan-in
+// > 129) are split at numpy's pairwise-tree leaves and finished by
+// combine_kernel in tree order. Column chunks are the slow grid dimension,
+// so all items of chunk 0 run before chunk 1: the previous layer's working
+// set per chunk is W_prev x 512 B (35 MB at the widest layer of config C),
+// which stays L2-resident while its rows are gathered ~2.7 times each.
 #pragma once
 
 #include "common.cuh"
@@ -30,7 +25,7 @@ constexpr int WARPS_PER_BLOCK = 4;
 
 template <typename T>
 struct FwdGather {
-  static constexpr int NOP = 1, NX = 0, EB = 8;
+  static constexpr int NOP = 1, NX = 0, SE = 16;
   const T* base;
   long long ld;
   __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col) : base(a.prev + col), ld(a.ld) {}
@@ -51,7 +46,7 @@ template <typename T, int MODE>
 struct BwdGather {
   static constexpr int NOP = (MODE == BW_PASS) ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
-  static constexpr int EB = (MODE == BW_PASS) ? 8 : 4;
+  static constexpr int SE = 8;
   const T* gbase;
   const T* nbase;
   const T* xbase;
@@ -125,132 +120,251 @@ struct BwdGather {
 };
 
 // ---- the work-item kernel ----------------------------------------------------
+//
+// Item kinds (int4 {x, y, z, w}, built by klay.cu build_items):
+//   short task   y > 0   nodes [x, y), edges [z, w): whole segments of at most
+//                        G::SE edges each; staged in node-aligned batches of
+//                        <= SE edges and reduced node by node
+//   long segment y == 0  node x, edges [z, w): one segment, x0 = edge z and the
+//                        tail in rounds of 8 aligned with numpy's 8-way
+//                        pairwise accumulators (statically indexed registers)
+//   leaf         y < 0   one pairwise leaf [z, w) of node x's tail; the partial
+//                        goes to scratch slot -y-1 (combine_kernel finishes)
+// Every lane owns one 16-byte column vector; rows are staged with cp.async
+// into a double-buffered per-warp shared-memory stage, so a warp keeps up to
+// two batches of 512-byte row chunks in flight with no register cost.
+
+constexpr int TASK_EDGES = 128;  // max edges of a short task (indices staged in smem)
+constexpr int TASK_NODES = 128;  // max nodes of a short task
+
+template <typename T, typename G>
+struct ItemsSmem {
+  static constexpr int SE = G::SE;                 // edges per stage batch
+  static constexpr int EV = G::NOP * 32;           // Vec<T> per staged edge
+  static constexpr int XV = G::NX * 32;            // Vec<T> per staged own value
+  static constexpr int STAGE_V = SE * (EV + XV);   // Vec<T> per stage
+  static constexpr size_t warp_bytes =
+      ((size_t)2 * STAGE_V * sizeof(Vec<T>) + (size_t)(TASK_EDGES + TASK_NODES + 1) * sizeof(int) +
+       127) / 128 * 128;
+  static constexpr size_t bytes = warp_bytes * WARPS_PER_BLOCK;
+};
 
 template <typename T, int RK>
-struct OpFor { using type = SeqOp<T, RK>; };
-template <typename T>
-struct OpFor<T, RK_SUM> { using type = SumOp<T>; };
-template <typename T>
-struct OpFor<T, RK_LSE> { using type = LseOp<T>; };
+__device__ __forceinline__ void seq_combine(Vec<T>& acc, const Vec<T>& x) {
+#pragma unroll
+  for (int c = 0; c < Vec<T>::N; ++c) {
+    if constexpr (RK == RK_PROD) acc.v[c] = acc.v[c] * x.v[c];
+    else if constexpr (RK == RK_MAX) acc.v[c] = npmax(acc.v[c], x.v[c]);
+    else acc.v[c] = npmin(acc.v[c], x.v[c]);
+  }
+}
 
-constexpr int ITEM_IDX = 128;  // edge indices staged per item (longer items read idx directly)
-
-template <typename T, int RK, typename G>
-struct ItemsSmem {
-  static constexpr int SLOT = (G::NOP + G::NX) * 32;  // Vec<T> per edge slot
-  static constexpr size_t stage = (size_t)WARPS_PER_BLOCK * 2 * G::EB * SLOT * sizeof(Vec<T>);
-  static constexpr size_t accum = (RK == RK_SUM) ? (size_t)8 * WARPS_PER_BLOCK * 32 * sizeof(Vec<T>) : 0;
-  static constexpr size_t index = (size_t)WARPS_PER_BLOCK * (ITEM_IDX + 32) * sizeof(int);
-  static constexpr size_t bytes = stage + accum + index;
-};
+template <typename T>
+__device__ __forceinline__ Vec<T> combine8(const Vec<T> (&r)[8]) {
+  Vec<T> res;
+#pragma unroll
+  for (int c = 0; c < Vec<T>::N; ++c)
+    res.v[c] = ((r[0].v[c] + r[1].v[c]) + (r[2].v[c] + r[3].v[c])) +
+               ((r[4].v[c] + r[5].v[c]) + (r[6].v[c] + r[7].v[c]));
+  return res;
+}
 
 template <typename T, int RK, typename G>
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T> a) {
-  using Op = typename OpFor<T, RK>::type;
-  using S = ItemsSmem<T, RK, G>;
-  constexpr int EB = G::EB, SLOT = S::SLOT;
+  using S = ItemsSmem<T, G>;
+  constexpr int SE = S::SE, EV = S::EV, XV = S::XV, STAGE_V = S::STAGE_V;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
   if (item >= a.n_items) return;  // no block-wide barriers below
-  Vec<T>* stage = reinterpret_cast<Vec<T>*>(smem) + (size_t)warp * 2 * EB * SLOT;
-  int* widx = reinterpret_cast<int*>(smem + S::stage + S::accum) + warp * (ITEM_IDX + 32);
-  int* wend = widx + ITEM_IDX;
+  unsigned char* wbase = smem + (size_t)warp * S::warp_bytes;
+  Vec<T>* stage = reinterpret_cast<Vec<T>*>(wbase);
+  int* widx = reinterpret_cast<int*>(wbase + (size_t)2 * STAGE_V * sizeof(Vec<T>));
+  int* woff = widx + TASK_EDGES;
 
   const int v = blockIdx.y * 32 + lane;
   const bool active = v < a.V;
   const size_t col = (size_t)v * Vec<T>::N;
   const long long ld = a.ld;
   const int4 it = __ldg(a.items + item);
-  const bool leaf = it.y < 0;
-  const int nn = leaf ? 1 : it.y - it.x;
   const int ne = it.w - it.z;
-  const bool staged_idx = ne <= ITEM_IDX;
   const G g(a, col);
-  Op op;
-  if constexpr (RK == RK_LSE) op.eps = a.eps;
-  if constexpr (RK == RK_SUM) {
-    op.r = reinterpret_cast<Vec<T>*>(smem + S::stage) + threadIdx.x;
-    op.rstride = WARPS_PER_BLOCK * 32;
-  }
-  // the item's edge indices and (relative) segment ends, one round trip
+  const bool staged_idx = ne <= TASK_EDGES;
   if (staged_idx)
     for (int q = lane; q < ne; q += 32) widx[q] = __ldg(a.idx + it.z + q);
-  if (!leaf && lane < nn) wend[lane] = __ldg(a.off + it.x + 1 + lane) - it.z;
-  __syncwarp();
 
-  // stage batch b: operand rows of edges [b*EB, b*EB+cnt) and the own value
-  // of every node whose segment starts in the batch
-  int xnode = 0, xstart = 0;
-  auto issue = [&](int b) {
-    const int base = b * EB;
-    const int cnt = min(EB, ne - base);
-    Vec<T>* st = stage + (b & 1) * EB * SLOT;
-    if (active) {
-      for (int i = 0; i < cnt; ++i) {
-        const int row = staged_idx ? widx[base + i] : __ldg(a.idx + it.z + base + i);
-        g.issue(st + i * SLOT, row, lane);
+  if (it.y > 0) {
+    // ======================= short task =======================
+    const int nb = it.x, nn = it.y - it.x;
+    for (int q = lane; q <= nn; q += 32) woff[q] = __ldg(a.off + nb + q) - it.z;
+    __syncwarp();
+    // node-aligned batch [n0, n1) with at most SE edges
+    auto batch_end = [&](int n0) {
+      int n1 = n0 + 1;
+      const int lim = woff[n0] + SE;
+      while (n1 < nn && woff[n1 + 1] <= lim) ++n1;
+      return n1;
+    };
+    auto issue = [&](int n0, int n1, int s) {
+      Vec<T>* st = stage + s * STAGE_V;
+      const int eb = woff[n0], cnt = woff[n1] - eb;
+      if (active) {
+        for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, widx[eb + i], lane);
+        if constexpr (G::NX)
+          for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nb + nd, lane);
       }
-    }
-    if constexpr (G::NX) {
-      if (leaf) {
-        if (b == 0 && active) g.issue_x(st + G::NOP * 32, it.x, lane);
+      cp_async_commit();
+    };
+    int n0 = 0, n1 = batch_end(0), s = 0;
+    issue(n0, n1, 0);
+    while (n0 < nn) {
+      const int m0 = n1, m1 = (m0 < nn) ? batch_end(m0) : m0;
+      if (m0 < nn) {
+        issue(m0, m1, s ^ 1);
+        cp_async_wait<1>();
       } else {
-        while (xnode < nn && xstart < base + cnt) {
-          if (active) g.issue_x(st + (xstart - base) * SLOT + G::NOP * 32, it.x + xnode, lane);
-          xstart = wend[xnode];
-          ++xnode;
+        cp_async_wait<0>();
+      }
+      if (active) {
+        const Vec<T>* st = stage + s * STAGE_V;
+        const int eb = woff[n0];
+        for (int nd = n0; nd < n1; ++nd) {
+          const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
+          Vec<T> x{};
+          if constexpr (G::NX) x = st[SE * EV + (nd - n0) * XV + lane];
+          auto val = [&](int e) { return g.value(st + e * EV, lane, widx[eb + e], x); };
+          Vec<T> out;
+          if constexpr (RK == RK_SUM) {
+            // x0 + numpy pairwise(tail), tail < 16 elements
+            out = val(sb);
+            if (n > 1) {
+              Vec<T> res;
+              int j = 1;
+              if (n <= 8) {
+                res = vfill<T>(T(-0.0));
+              } else {
+                Vec<T> r[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = val(sb + 1 + k);
+                res = combine8(r);
+                j = 9;
+              }
+              for (; j < n; ++j) res = vadd(res, val(sb + j));
+              out = vadd(out, res);
+            }
+          } else if constexpr (RK == RK_LSE) {
+            LseOp<T> op;
+            op.eps = a.eps;
+            op.begin(n);
+            for (int j = 0; j < n; ++j) op.push(val(sb + j));
+            out = op.result();
+          } else {
+            out = val(sb);
+            for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
+          }
+          stv(a.out + (size_t)(nb + nd) * ld + col, out);
         }
       }
+      n0 = m0;
+      n1 = m1;
+      s ^= 1;
+    }
+    return;
+  }
+
+  // ===================== long segment / leaf =====================
+  __syncwarp();
+  const bool leaf = it.y < 0;
+  const int node = it.x;
+  const int t0 = leaf ? 0 : 1;      // first tail edge (relative)
+  const int m = ne - t0;            // tail length
+  Vec<T> x{};
+  if constexpr (G::NX) x = g.load_x(node);
+  auto row_of = [&](int e) { return staged_idx ? widx[e] : __ldg(a.idx + it.z + e); };
+  // round t stages tail elements [8t, 8t+8)
+  auto issue = [&](int t, int s) {
+    Vec<T>* st = stage + s * STAGE_V;
+    const int base = t0 + 8 * t;
+    const int cnt = min(8, ne - base);
+    const int my_row = (lane < cnt) ? row_of(base + lane) : 0;
+    for (int i = 0; i < cnt; ++i) {
+      const int row = __shfl_sync(0xffffffffu, my_row, i);
+      if (active) g.issue(st + i * EV, row, lane);
     }
     cp_async_commit();
   };
-
-  const int nb = (ne + EB - 1) / EB;
-  int node = 0, seg_start = 0;
-  int seg_end = leaf ? ne : wend[0];
-  if (leaf) op.begin_leaf(ne);
-  else op.begin(seg_end);
-  Vec<T> x{};
-  issue(0);
-  for (int b = 0; b < nb; ++b) {
-    if (b + 1 < nb) {
-      issue(b + 1);
+  const int nr = (m + 7) / 8;
+  Vec<T> x0{};
+  if (!leaf && active) x0 = g.direct(row_of(0), x);
+  if (nr > 0) issue(0, 0);
+  const int mainend = m - (m & 7);
+  Vec<T> r[8];
+  Vec<T> res = vfill<T>(T(-0.0));  // SUM tail accumulator
+  Vec<T> acc = x0;                 // SEQ accumulator
+  LseOp<T> lse;
+  if constexpr (RK == RK_LSE) {
+    lse.eps = a.eps;
+    lse.begin(ne);
+    if (!leaf) lse.push(x0);
+  }
+  bool have = !leaf;               // SEQ: acc holds a value
+  for (int t = 0; t < nr; ++t) {
+    const int s = t & 1;
+    if (t + 1 < nr) {
+      issue(t + 1, s ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    const Vec<T>* st = stage + (b & 1) * EB * SLOT;
-    const int base = b * EB;
-    const int cnt = min(EB, ne - base);
-    for (int i = 0; i < cnt; ++i) {
-      const int k = base + i;
-      if constexpr (G::NX) {
-        if (k == seg_start && (!leaf || k == 0)) x = st[i * SLOT + G::NOP * 32 + lane];
+    if (!active) continue;
+    const Vec<T>* st = stage + s * STAGE_V;
+    const int base = t0 + 8 * t;
+    const int cnt = min(8, ne - base);
+    auto val = [&](int i) { return g.value(st + i * EV, lane, (G::NOP == 2) ? row_of(base + i) : 0, x); };
+    if constexpr (RK == RK_SUM) {
+      if (m >= 8 && 8 * t < mainend) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const Vec<T> xv = val(k);
+          r[k] = (t == 0) ? xv : vadd(r[k], xv);
+        }
+      } else {
+        if (m >= 8 && 8 * t == mainend) res = combine8(r);
+        for (int i = 0; i < cnt; ++i) res = vadd(res, val(i));
       }
-      if (active) {
-        const int row = (G::NX && G::NOP == 2) ? (staged_idx ? widx[k] : __ldg(a.idx + it.z + k)) : 0;
-        op.push(g.value(st + i * SLOT, lane, row, x));
-      }
-      if (!leaf && k + 1 == seg_end) {
-        if (active) stv(a.out + (size_t)(it.x + node) * ld + col, op.result());
-        ++node;
-        if (node < nn) {
-          seg_start = seg_end;
-          seg_end = wend[node];
-          op.begin(seg_end - seg_start);
+    } else if constexpr (RK == RK_LSE) {
+      for (int i = 0; i < cnt; ++i) lse.push(val(i));
+    } else {
+      for (int i = 0; i < cnt; ++i) {
+        if (!have) {
+          acc = val(i);
+          have = true;
+        } else {
+          seq_combine<T, RK>(acc, val(i));
         }
       }
     }
   }
-  if (leaf && active) {
+  if (!active) return;
+  if constexpr (RK == RK_SUM) {
+    if (m >= 8 && mainend == m) res = combine8(r);
+  }
+  if (leaf) {
     const int slot = -it.y - 1;
     if constexpr (RK == RK_LSE) {
-      stv(a.scratch + (size_t)slot * ld + col, op.m);
-      stv(a.scratch + a.tpart + (size_t)slot * ld + col, op.t);
+      stv(a.scratch + (size_t)slot * ld + col, lse.m);
+      stv(a.scratch + a.tpart + (size_t)slot * ld + col, lse.t);
+    } else if constexpr (RK == RK_SUM) {
+      stv(a.scratch + (size_t)slot * ld + col, res);
     } else {
-      stv(a.scratch + (size_t)slot * ld + col, op.partial());
+      stv(a.scratch + (size_t)slot * ld + col, acc);
     }
+  } else {
+    Vec<T> out;
+    if constexpr (RK == RK_SUM) out = (m == 0) ? x0 : vadd(x0, res);
+    else if constexpr (RK == RK_LSE) out = lse.result();
+    else out = acc;
+    stv(a.out + (size_t)node * ld + col, out);
   }
 }
 
@@ -302,7 +416,7 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
   int launched = 0;
   if (a.n_items > 0) {
     ++launched;
-    constexpr size_t smem = ItemsSmem<T, RK, G>::bytes;
+    constexpr size_t smem = ItemsSmem<T, G>::bytes;
     static bool configured = false;  // opt in to > 48 KB dynamic smem once per kernel
     if (!configured) {
       cudaFuncSetAttribute(items_kernel<T, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
