@@ -23,9 +23,9 @@ enum { SR_REAL_ = 0, SR_LOG_ = 1 };
 enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2 };
 
 // work-item shape (see layer_kernels.cuh)
-constexpr int TASK_EDGES_H = 128;  // edges per short task (== TASK_EDGES)
-constexpr int TASK_NODES_H = 128;  // nodes per short task (== TASK_NODES)
-constexpr int SHORT_FWD = 16;      // FwdGather::SE
+constexpr int TASK_EDGES_H = 64;   // edges per short task (<= TASK_EDGES)
+constexpr int TASK_NODES_H = 32;   // nodes per short task (<= TASK_NODES)
+constexpr int SHORT_FWD = 8;       // FwdGather::SE
 constexpr int SHORT_BWD = 8;       // BwdGather::SE
 constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are split
 

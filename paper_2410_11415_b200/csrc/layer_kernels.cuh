@@ -25,7 +25,7 @@ constexpr int WARPS_PER_BLOCK = 4;
 
 template <typename T>
 struct FwdGather {
-  static constexpr int NOP = 1, NX = 0, SE = 16;
+  static constexpr int NOP = 1, NX = 0, SE = 8;
   const T* base;
   long long ld;
   __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col) : base(a.prev + col), ld(a.ld) {}
@@ -421,6 +421,12 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
     if (!configured) {
       cudaFuncSetAttribute(items_kernel<T, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
+      // one carveout for every layer kernel: consecutive launches never wait
+      // for an L1/shared-memory reconfiguration of the SMs
+      cudaFuncSetAttribute(items_kernel<T, RK, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(combine_kernel<T, RK, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
       configured = true;
     }
     dim3 grid((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
