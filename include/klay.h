@@ -132,7 +132,8 @@ int64_t klay_launch_count(void);
 /* Time every subsequent launch of this thread with CUDA events on its
  * stream until klay_profiler_end (which synchronizes). Record kinds:
  * 0 = forward layer kernel, 1 = backward layer kernel, 2 = forward
- * boundary (inputs / outputs), 3 = backward boundary (seeds / grads);
+ * boundary (inputs / outputs), 3 = backward boundary (seeds / grads),
+ * 4 / 5 = forward / backward persistent tail (all layers >= `layers`);
  * `layers` holds the 1-based gate layer (0 / L+1 for boundary kernels). */
 int klay_profiler_begin(void);
 int klay_profiler_end(int32_t max_records, int32_t* kinds, int32_t* layers, float* ms,

@@ -32,14 +32,16 @@ struct alignas(16) Vec {
   T v[N];
 };
 
+// Value loads go through L2 (ld.global.cg), never the non-coherent path:
+// the persistent tail kernel reads rows written earlier in the same launch.
 __device__ __forceinline__ Vec<float> ldv(const float* p) {
-  float4 u = __ldg(reinterpret_cast<const float4*>(p));
+  float4 u = __ldcg(reinterpret_cast<const float4*>(p));
   Vec<float> r;
   r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
   return r;
 }
 __device__ __forceinline__ Vec<double> ldv(const double* p) {
-  double2 u = __ldg(reinterpret_cast<const double2*>(p));
+  double2 u = __ldcg(reinterpret_cast<const double2*>(p));
   Vec<double> r;
   r.v[0] = u.x; r.v[1] = u.y;
   return r;

@@ -24,10 +24,20 @@ enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2 };
 
 // work-item shape (see layer_kernels.cuh)
 constexpr int TASK_EDGES_H = 64;   // edges per short task (<= TASK_EDGES)
-constexpr int TASK_NODES_H = 32;   // nodes per short task (<= TASK_NODES)
+constexpr int TASK_NODES_H = 31;   // nodes per short task (<= TASK_NODES)
 constexpr int SHORT_FWD = 8;       // FwdGather::SE
 constexpr int SHORT_BWD = 8;       // BwdGather::SE
 constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are split
+// persistent tail (layer_kernels.cuh tail_kernel): the suffix of layers with
+// at most TAIL_EDGES edges runs in one launch per direction
+constexpr int TAIL_EDGES = 4096;
+constexpr int TAIL_CLUSTER = 8;     // CTAs per cluster (one cluster per column chunk)
+constexpr int TAIL_WARPS_H = 8;     // warps per CTA (== TAIL_WARPS)
+
+const bool g_no_tail = [] {
+  const char* e = getenv("KLAY_NO_TAIL");
+  return e && *e && *e != '0';
+}();
 
 thread_local std::string g_err;
 
@@ -111,9 +121,9 @@ void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
 // cap shrinks for narrow layers so that thin layers still spread over many
 // warps (short per-warp dependency chains).
 void build_items(const std::vector<int>& off, size_t base, int W, int short_max, ItemSet& s,
-                 bool split = true) {
+                 bool split = true, int cap = 0) {
   const int E = off[base + W] - off[base];
-  const int cap = std::max(short_max, std::min(TASK_EDGES_H, (E / 296) & ~7));
+  if (cap <= 0) cap = std::max(short_max, std::min(TASK_EDGES_H, (E / 296) & ~7));
   std::vector<int4> leaves, longs, shorts;
   std::vector<std::pair<int, int>> lv;
   int tb = -1, t_edges = 0;
@@ -195,6 +205,7 @@ struct KlayPlan {
   int* d_top_off = nullptr;
   int* d_top_pos = nullptr;
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
+  int32_t tail_from = 0;  // first layer of the persistent tail (L = no tail)
 };
 
 extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
@@ -246,6 +257,12 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
 
   std::vector<int> off, src, toff, tpar;
   std::vector<int4> items, heavy;
+  // the tail: longest suffix of layers with <= TAIL_EDGES edges
+  int32_t tail_from = num_layers;
+  while (tail_from > 0 && num_layers - tail_from < TAIL_MAX_LAYERS &&
+         edge_counts[tail_from - 1] <= TAIL_EDGES)
+    --tail_from;
+  p->tail_from = tail_from;
   int64_t prev_w = num_inputs, row = num_inputs, e_base = 0;
   p->max_width = num_inputs;
   p->layer_row.push_back(0);
@@ -302,8 +319,13 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     for (int64_t e = 0; e < E; ++e) tpar[tb + pos[S[e]]++] = (int)G[e];
     // work items: forward over parents, backward over children
     ItemSet fs, bs;
-    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs);
-    build_items(toff, (size_t)d.toff_base, (int)prev_w, SHORT_BWD, bs);
+    // tail layers: about one item per cluster warp (fewer, larger items)
+    const int tcap = (l >= tail_from)
+        ? std::max(8, std::min(TASK_EDGES_H, (int)((E + TAIL_CLUSTER * TAIL_WARPS_H - 1) /
+                                                   (TAIL_CLUSTER * TAIL_WARPS_H) + 7) & ~7))
+        : 0;
+    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap);
+    build_items(toff, (size_t)d.toff_base, (int)prev_w, SHORT_BWD, bs, true, tcap);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
@@ -311,7 +333,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.fq_n = d.fi_n;
     if (d.prod && !fs.heavy.empty()) {
       ItemSet qs;
-      build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, qs, false);
+      build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, qs, false, tcap);
       d.fq_base = (int64_t)items.size();
       d.fq_n = (int64_t)qs.items.size();
       items.insert(items.end(), qs.items.begin(), qs.items.end());
@@ -418,6 +440,7 @@ LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, 
   a.ld = ld;
   a.foff = p->d_off + d.off_base;
   a.fsrc = p->d_src + d.e_base;
+  a.prod = d.prod ? 1 : 0;
   return a;
 }
 
@@ -433,6 +456,13 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     ++g_launches;
   }
   const T* prev = values;
+  const int chunks = (V + 31) / 32;
+  const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
+  TailArgs<T>* tail = nullptr;
+  if (tail_from < p->L) {
+    tail = new TailArgs<T>();
+    tail->n = 0;
+  }
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
@@ -448,9 +478,21 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     a.eps = (T)eps;
     a.scratch = work;
     a.tpart = (long long)p->max_fslots * ld;
-    LaunchScope ls(s, 0, l + 1);
-    g_launches += launch_forward_layer(sr, d.prod, a, s);
+    if (l >= tail_from) {
+      tail->layer[tail->n++] = a;
+    } else {
+      LaunchScope ls(s, 0, l + 1);
+      g_launches += launch_forward_layer(sr, d.prod, a, s);
+    }
     prev = cur;
+  }
+  if (tail) {
+    LaunchScope ls(s, 4, tail_from + 1);
+    const int n = launch_forward_tail(sr, *tail, chunks, TAIL_CLUSTER, s);
+    delete tail;
+    if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
+                                            cudaGetErrorString(cudaGetLastError()));
+    g_launches += n;
   }
   if (outputs && p->R > 0) {
     const T zero = (sr == SR_LOG_) ? T(-INFINITY) : T(0);
@@ -475,6 +517,13 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     launch_seed<T>(seed, p->d_top_off, p->d_top_pos, g[cur], (int)p->WL, p->R, B, ld, s);
     ++g_launches;
   }
+  const int chunks = (V + 31) / 32;
+  const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
+  TailArgs<T>* tail = nullptr;
+  if (tail_from < p->L) {
+    tail = new TailArgs<T>();
+    tail->n = 0;
+  }
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
     LayerArgs<T> a = layer_args<T>(p, d, false, V, ld);
@@ -483,11 +532,24 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.ncur = trace + (size_t)d.row * ld;
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
-    int mode = BW_PASS_;
-    if (domain == SR_REAL_ && d.prod) mode = BW_REALPROD_;
-    else if (domain == SR_LOG_ && !d.prod) mode = BW_LOGSUM_;
-    LaunchScope ls(s, 1, l + 1);
-    g_launches += launch_backward_layer(mode, a, s);
+    if (l >= tail_from) {
+      tail->layer[tail->n++] = a;
+      if (l == tail_from) {
+        LaunchScope ls(s, 5, tail_from + 1);
+        const int n = launch_backward_tail(domain, *tail, chunks, TAIL_CLUSTER, s);
+        delete tail;
+        tail = nullptr;
+        if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
+                                                cudaGetErrorString(cudaGetLastError()));
+        g_launches += n;
+      }
+    } else {
+      int mode = BW_PASS_;
+      if (domain == SR_REAL_ && d.prod) mode = BW_REALPROD_;
+      else if (domain == SR_LOG_ && !d.prod) mode = BW_LOGSUM_;
+      LaunchScope ls(s, 1, l + 1);
+      g_launches += launch_backward_layer(mode, a, s);
+    }
     cur ^= 1;
   }
   if (p->K > 0) {

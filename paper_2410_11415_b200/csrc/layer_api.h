@@ -28,6 +28,16 @@ struct LayerArgs {
   const T* nprev;     // forward values of the children (own value x)
   const int* foff;    // forward CSR (real-product zero path)
   const int* fsrc;
+  int prod;           // product layer (selects the reduction in the tail kernel)
+};
+
+// The persistent tail kernel (thin upper layers in one launch) takes its
+// per-layer arguments by value as a __grid_constant__ kernel parameter.
+constexpr int TAIL_MAX_LAYERS = 96;
+template <typename T>
+struct TailArgs {
+  LayerArgs<T> layer[TAIL_MAX_LAYERS];
+  int n;
 };
 
 // forward layer: semiring x layer op -> reduction kind (RK_*)
@@ -36,6 +46,13 @@ int launch_forward_layer(int sr, bool prod, const LayerArgs<double>& a, cudaStre
 // backward layer (BW_* mode): always a pairwise sum over each child's out-edges
 int launch_backward_layer(int mode, const LayerArgs<float>& a, cudaStream_t s);
 int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s);
+
+// persistent tail: layers t.layer[0..n) in order, one cluster per column
+// chunk; returns the number of kernels launched (0 on a launch failure)
+int launch_forward_tail(int sr, const TailArgs<float>& t, int chunks, int cluster, cudaStream_t s);
+int launch_forward_tail(int sr, const TailArgs<double>& t, int chunks, int cluster, cudaStream_t s);
+int launch_backward_tail(int domain, const TailArgs<float>& t, int chunks, int cluster, cudaStream_t s);
+int launch_backward_tail(int domain, const TailArgs<double>& t, int chunks, int cluster, cudaStream_t s);
 
 // boundary kernels
 template <typename T>

@@ -9,6 +9,8 @@
 // which stays L2-resident while its rows are gathered ~2.7 times each.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "layer_api.h"
 
@@ -134,18 +136,18 @@ struct BwdGather {
 // into a double-buffered per-warp shared-memory stage, so a warp keeps up to
 // two batches of 512-byte row chunks in flight with no register cost.
 
-constexpr int TASK_EDGES = 128;  // max edges of a short task (indices staged in smem)
-constexpr int TASK_NODES = 128;  // max nodes of a short task
+constexpr int TASK_EDGES = 128;  // max staged edge indices per item (longer items read idx directly)
+constexpr int TASK_NODES = 31;   // max nodes of a short task (one lane per segment offset)
 
 template <typename T, typename G>
 struct ItemsSmem {
-  static constexpr int SE = G::SE;                 // edges per stage batch
+  static constexpr int SE = G::SE;                 // edges per stage batch (= max short segment)
   static constexpr int EV = G::NOP * 32;           // Vec<T> per staged edge
   static constexpr int XV = G::NX * 32;            // Vec<T> per staged own value
   static constexpr int STAGE_V = SE * (EV + XV);   // Vec<T> per stage
+  static constexpr int IDX_INTS = TASK_EDGES + 32 + 33;  // widx | woff | wbat
   static constexpr size_t warp_bytes =
-      ((size_t)2 * STAGE_V * sizeof(Vec<T>) + (size_t)(TASK_EDGES + TASK_NODES + 1) * sizeof(int) +
-       127) / 128 * 128;
+      ((size_t)2 * STAGE_V * sizeof(Vec<T>) + (size_t)IDX_INTS * sizeof(int) + 127) / 128 * 128;
   static constexpr size_t bytes = warp_bytes * WARPS_PER_BLOCK;
 };
 
@@ -169,105 +171,103 @@ __device__ __forceinline__ Vec<T> combine8(const Vec<T> (&r)[8]) {
   return res;
 }
 
+// One work item for one 512-byte column chunk, processed by one warp with
+// its own slice `wbase` of shared memory (ItemsSmem::warp_bytes).
 template <typename T, int RK, typename G>
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T> a) {
+__device__ __forceinline__ void process_item(const LayerArgs<T>& a, int item, int chunk,
+                                             unsigned char* wbase, int lane) {
   using S = ItemsSmem<T, G>;
   constexpr int SE = S::SE, EV = S::EV, XV = S::XV, STAGE_V = S::STAGE_V;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
-  if (item >= a.n_items) return;  // no block-wide barriers below
-  unsigned char* wbase = smem + (size_t)warp * S::warp_bytes;
   Vec<T>* stage = reinterpret_cast<Vec<T>*>(wbase);
   int* widx = reinterpret_cast<int*>(wbase + (size_t)2 * STAGE_V * sizeof(Vec<T>));
   int* woff = widx + TASK_EDGES;
+  int* wbat = woff + 32;
 
-  const int v = blockIdx.y * 32 + lane;
+  // Lanes past the row (v >= V) work on column 0 and never store: the whole
+  // warp runs the same instruction stream without divergence.
+  const int v = chunk * 32 + lane;
   const bool active = v < a.V;
-  const size_t col = (size_t)v * Vec<T>::N;
+  const size_t col = (size_t)(active ? v : 0) * Vec<T>::N;
   const long long ld = a.ld;
   const int4 it = __ldg(a.items + item);
   const int ne = it.w - it.z;
   const G g(a, col);
   const bool staged_idx = ne <= TASK_EDGES;
+  // a warp may run several items back to back (tail kernel): every lane must
+  // be done with the previous item's shared index arrays before they change
+  __syncwarp();
   if (staged_idx)
     for (int q = lane; q < ne; q += 32) widx[q] = __ldg(a.idx + it.z + q);
 
   if (it.y > 0) {
     // ======================= short task =======================
+    // nodes [nb, nb+nn), every segment <= SE edges; node-aligned batches of
+    // <= SE edges are staged two at a time and reduced node by node
     const int nb = it.x, nn = it.y - it.x;
-    for (int q = lane; q <= nn; q += 32) woff[q] = __ldg(a.off + nb + q) - it.z;
+    if (lane <= nn) woff[lane] = __ldg(a.off + nb + lane) - it.z;
     __syncwarp();
-    // node-aligned batch [n0, n1) with at most SE edges
-    auto batch_end = [&](int n0) {
-      int n1 = n0 + 1;
-      const int lim = woff[n0] + SE;
-      while (n1 < nn && woff[n1 + 1] <= lim) ++n1;
-      return n1;
-    };
-    auto issue = [&](int n0, int n1, int s) {
-      Vec<T>* st = stage + s * STAGE_V;
-      const int eb = woff[n0], cnt = woff[n1] - eb;
-      if (active) {
-        for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, widx[eb + i], lane);
-        if constexpr (G::NX)
-          for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nb + nd, lane);
+    int nbat = 0;
+    if (lane == 0) {
+      int n0 = 0;
+      wbat[0] = 0;
+      while (n0 < nn) {
+        const int lim = woff[n0] + SE;
+        int n1 = n0 + 1;
+        while (n1 < nn && woff[n1 + 1] <= lim) ++n1;
+        wbat[++nbat] = n1;
+        n0 = n1;
       }
+    }
+    nbat = __shfl_sync(0xffffffffu, nbat, 0);
+    __syncwarp();
+    auto issue = [&](int b) {
+      Vec<T>* st = stage + (b & 1) * STAGE_V;
+      const int n0 = wbat[b], n1 = wbat[b + 1];
+      const int eb = woff[n0], cnt = woff[n1] - eb;
+      for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, widx[eb + i], lane);
+      if constexpr (G::NX)
+        for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nb + nd, lane);
       cp_async_commit();
     };
-    int n0 = 0, n1 = batch_end(0), s = 0;
-    issue(n0, n1, 0);
-    while (n0 < nn) {
-      const int m0 = n1, m1 = (m0 < nn) ? batch_end(m0) : m0;
-      if (m0 < nn) {
-        issue(m0, m1, s ^ 1);
+    T* outp = a.out + (size_t)nb * ld + col;
+    issue(0);
+    for (int b = 0; b < nbat; ++b) {
+      if (b + 1 < nbat) {
+        issue(b + 1);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
-      if (active) {
-        const Vec<T>* st = stage + s * STAGE_V;
-        const int eb = woff[n0];
-        for (int nd = n0; nd < n1; ++nd) {
-          const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
-          Vec<T> x{};
-          if constexpr (G::NX) x = st[SE * EV + (nd - n0) * XV + lane];
-          auto val = [&](int e) { return g.value(st + e * EV, lane, widx[eb + e], x); };
-          Vec<T> out;
-          if constexpr (RK == RK_SUM) {
-            // x0 + numpy pairwise(tail), tail < 16 elements
-            out = val(sb);
-            if (n > 1) {
-              Vec<T> res;
-              int j = 1;
-              if (n <= 8) {
-                res = vfill<T>(T(-0.0));
-              } else {
-                Vec<T> r[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) r[k] = val(sb + 1 + k);
-                res = combine8(r);
-                j = 9;
-              }
-              for (; j < n; ++j) res = vadd(res, val(sb + j));
-              out = vadd(out, res);
-            }
-          } else if constexpr (RK == RK_LSE) {
-            LseOp<T> op;
-            op.eps = a.eps;
-            op.begin(n);
-            for (int j = 0; j < n; ++j) op.push(val(sb + j));
-            out = op.result();
-          } else {
-            out = val(sb);
-            for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
+      const Vec<T>* st = stage + (b & 1) * STAGE_V;
+      const int n0 = wbat[b], n1 = wbat[b + 1];
+      const int eb = woff[n0];
+      for (int nd = n0; nd < n1; ++nd) {
+        const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
+        Vec<T> x{};
+        if constexpr (G::NX) x = st[SE * EV + (nd - n0) * XV + lane];
+        auto val = [&](int e) {
+          return g.value(st + e * EV, lane, (G::NOP == 2) ? widx[eb + e] : 0, x);
+        };
+        Vec<T> out = val(sb);
+        if constexpr (RK == RK_SUM) {
+          // x0 + (-0 + x1 + ... + x_{n-1}): n <= 8 keeps numpy's sequential branch
+          if (n > 1) {
+            Vec<T> acc = val(sb + 1);
+            for (int j = 2; j < n; ++j) acc = vadd(acc, val(sb + j));
+            out = vadd(out, acc);
           }
-          stv(a.out + (size_t)(nb + nd) * ld + col, out);
+        } else if constexpr (RK == RK_LSE) {
+          LseOp<T> op;
+          op.eps = a.eps;
+          op.begin(n);
+          op.push(out);
+          for (int j = 1; j < n; ++j) op.push(val(sb + j));
+          out = op.result();
+        } else {
+          for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
         }
+        if (active) stv(outp + (size_t)nd * ld, out);
       }
-      n0 = m0;
-      n1 = m1;
-      s ^= 1;
     }
     return;
   }
@@ -282,21 +282,18 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T
   if constexpr (G::NX) x = g.load_x(node);
   auto row_of = [&](int e) { return staged_idx ? widx[e] : __ldg(a.idx + it.z + e); };
   // round t stages tail elements [8t, 8t+8)
-  auto issue = [&](int t, int s) {
-    Vec<T>* st = stage + s * STAGE_V;
+  auto issue = [&](int t) {
+    Vec<T>* st = stage + (t & 1) * STAGE_V;
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
     const int my_row = (lane < cnt) ? row_of(base + lane) : 0;
-    for (int i = 0; i < cnt; ++i) {
-      const int row = __shfl_sync(0xffffffffu, my_row, i);
-      if (active) g.issue(st + i * EV, row, lane);
-    }
+    for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, __shfl_sync(0xffffffffu, my_row, i), lane);
     cp_async_commit();
   };
   const int nr = (m + 7) / 8;
   Vec<T> x0{};
-  if (!leaf && active) x0 = g.direct(row_of(0), x);
-  if (nr > 0) issue(0, 0);
+  if (!leaf) x0 = g.direct(row_of(0), x);
+  if (nr > 0) issue(0);
   const int mainend = m - (m & 7);
   Vec<T> r[8];
   Vec<T> res = vfill<T>(T(-0.0));  // SUM tail accumulator
@@ -307,48 +304,43 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T
     lse.begin(ne);
     if (!leaf) lse.push(x0);
   }
-  bool have = !leaf;               // SEQ: acc holds a value
   for (int t = 0; t < nr; ++t) {
-    const int s = t & 1;
     if (t + 1 < nr) {
-      issue(t + 1, s ^ 1);
+      issue(t + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    if (!active) continue;
-    const Vec<T>* st = stage + s * STAGE_V;
+    const Vec<T>* st = stage + (t & 1) * STAGE_V;
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
-    auto val = [&](int i) { return g.value(st + i * EV, lane, (G::NOP == 2) ? row_of(base + i) : 0, x); };
+    auto val = [&](int i) {
+      return g.value(st + i * EV, lane, (G::NOP == 2) ? row_of(base + i) : 0, x);
+    };
     if constexpr (RK == RK_SUM) {
-      if (m >= 8 && 8 * t < mainend) {
+      if (8 * t < mainend) {
+        // a full round of numpy's 8 pairwise accumulators
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const Vec<T> xv = val(k);
           r[k] = (t == 0) ? xv : vadd(r[k], xv);
         }
       } else {
-        if (m >= 8 && 8 * t == mainend) res = combine8(r);
+        if (m >= 8) res = combine8(r);
         for (int i = 0; i < cnt; ++i) res = vadd(res, val(i));
       }
     } else if constexpr (RK == RK_LSE) {
       for (int i = 0; i < cnt; ++i) lse.push(val(i));
     } else {
-      for (int i = 0; i < cnt; ++i) {
-        if (!have) {
-          acc = val(i);
-          have = true;
-        } else {
-          seq_combine<T, RK>(acc, val(i));
-        }
-      }
+      int i = 0;
+      if (leaf && t == 0) acc = val(i++);
+      for (; i < cnt; ++i) seq_combine<T, RK>(acc, val(i));
     }
   }
-  if (!active) return;
   if constexpr (RK == RK_SUM) {
     if (m >= 8 && mainend == m) res = combine8(r);
   }
+  if (!active) return;
   if (leaf) {
     const int slot = -it.y - 1;
     if constexpr (RK == RK_LSE) {
@@ -368,13 +360,19 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T
   }
 }
 
+template <typename T, int RK, typename G>
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
+  if (item >= a.n_items) return;  // no block-wide barriers inside
+  process_item<T, RK, G>(a, item, blockIdx.y, smem + (size_t)warp * ItemsSmem<T, G>::warp_bytes, lane);
+}
+
 // ---- heavy-segment combine: x0 (+) leaf partials in order ---------------------
 
 template <typename T, int RK, typename G>
-__global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
-  const int h = blockIdx.x;
-  const int v = blockIdx.y * 32 + threadIdx.x;
-  if (h >= a.n_heavy || v >= a.V) return;
+__device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int v) {
   const size_t col = (size_t)v * Vec<T>::N;
   const long long ld = a.ld;
   const int4 hv = __ldg(a.heavy + h);
@@ -411,6 +409,14 @@ __global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
 }
 
 template <typename T, int RK, typename G>
+__global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
+  const int h = blockIdx.x;
+  const int v = blockIdx.y * 32 + threadIdx.x;
+  if (h >= a.n_heavy || v >= a.V) return;
+  process_heavy<T, RK, G>(a, h, v);
+}
+
+template <typename T, int RK, typename G>
 inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
   const unsigned chunks = (unsigned)((a.V + 31) / 32);
   int launched = 0;
@@ -438,6 +444,85 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
     combine_kernel<T, RK, G><<<grid, 32, 0, s>>>(a);
   }
   return launched;
+}
+
+// ---- persistent tail: all thin upper layers in one launch ---------------------
+//
+// One thread-block cluster per 512-byte column chunk (batch columns are
+// independent, so a cluster never waits for another); the cluster's warps
+// share each layer's work items and meet at a cluster barrier
+// (barrier.cluster arrive.release / wait.acquire) between layers. Values
+// written by one CTA are read by the others through L2 (cp.async.cg and
+// ld.global.cg), which the barrier's release/acquire ordering makes safe.
+
+constexpr int TAIL_WARPS = 8;
+
+template <typename T, typename GP, typename GS>
+struct TailSmem {
+  static constexpr size_t warp_bytes = ItemsSmem<T, GP>::warp_bytes > ItemsSmem<T, GS>::warp_bytes
+                                           ? ItemsSmem<T, GP>::warp_bytes
+                                           : ItemsSmem<T, GS>::warp_bytes;
+  static constexpr size_t bytes = warp_bytes * TAIL_WARPS;
+};
+
+template <typename T, int RKP, int RKS, typename GP, typename GS>
+__global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_constant__ TailArgs<T> t) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int csize = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int chunk = blockIdx.x / csize;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wbase = smem + (size_t)warp * TailSmem<T, GP, GS>::warp_bytes;
+  const int w = rank * TAIL_WARPS + warp, cw = csize * TAIL_WARPS;
+  for (int i = 0; i < t.n; ++i) {
+    const LayerArgs<T>& a = t.layer[i];
+    const int v = chunk * 32 + lane;
+    if (a.prod) {
+      for (int it = w; it < a.n_items; it += cw) process_item<T, RKP, GP>(a, it, chunk, wbase, lane);
+      if (a.n_heavy > 0) {
+        cluster.sync();
+        for (int h = w; h < a.n_heavy; h += cw)
+          if (v < a.V) process_heavy<T, RKP, GP>(a, h, v);
+      }
+    } else {
+      for (int it = w; it < a.n_items; it += cw) process_item<T, RKS, GS>(a, it, chunk, wbase, lane);
+      if (a.n_heavy > 0) {
+        cluster.sync();
+        for (int h = w; h < a.n_heavy; h += cw)
+          if (v < a.V) process_heavy<T, RKS, GS>(a, h, v);
+      }
+    }
+    cluster.sync();
+  }
+}
+
+template <typename T, int RKP, int RKS, typename GP, typename GS>
+inline int launch_tail(const TailArgs<T>& t, int chunks, int cluster, cudaStream_t s) {
+  auto kern = tail_kernel<T, RKP, RKS, GP, GS>;
+  constexpr size_t smem = TailSmem<T, GP, GS>::bytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(chunks * cluster), 1, 1);
+  cfg.blockDim = dim3(TAIL_WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, t) == cudaSuccess ? 1 : 0;
 }
 
 }  // namespace klay
