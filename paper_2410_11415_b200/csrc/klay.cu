@@ -30,9 +30,20 @@ constexpr int SHORT_BWD = 8;       // BwdGather::SE
 constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are split
 // persistent tail (layer_kernels.cuh tail_kernel): the suffix of layers with
 // at most TAIL_EDGES edges runs in one launch per direction
-constexpr int TAIL_EDGES = 4096;
-constexpr int TAIL_CLUSTER = 8;     // CTAs per cluster (one cluster per column chunk)
+const int TAIL_EDGES = [] {
+  const char* e = getenv("KLAY_TAIL_EDGES");
+  return (e && *e) ? atoi(e) : 2048;
+}();
+const int TAIL_CLUSTER = [] {       // CTAs per cluster (one cluster per column chunk)
+  const char* e = getenv("KLAY_TAIL_CLUSTER");
+  return (e && *e) ? atoi(e) : 8;
+}();
 constexpr int TAIL_WARPS_H = 8;     // warps per CTA (== TAIL_WARPS)
+
+const bool g_tail_debug = [] {
+  const char* e = getenv("KLAY_TAIL_DEBUG");
+  return e && *e && *e != '0';
+}();
 
 const bool g_no_tail = [] {
   const char* e = getenv("KLAY_NO_TAIL");
@@ -96,6 +107,7 @@ struct LaunchScope {
 
 struct ItemSet {
   std::vector<int4> items;
+  std::vector<unsigned> masks;  // parallel to items
   std::vector<int4> heavy;
   int slots = 0;
 };
@@ -125,11 +137,24 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   const int E = off[base + W] - off[base];
   if (cap <= 0) cap = std::max(short_max, std::min(TASK_EDGES_H, (E / 296) & ~7));
   std::vector<int4> leaves, longs, shorts;
+  std::vector<unsigned> short_masks;
   std::vector<std::pair<int, int>> lv;
   int tb = -1, t_edges = 0;
   auto flush = [&](int end_node) {
-    if (tb >= 0 && end_node > tb)
+    if (tb >= 0 && end_node > tb) {
       shorts.push_back(make_int4(tb, end_node, off[base + tb], off[base + end_node]));
+      // stage batches: greedy runs of whole segments with <= short_max edges
+      unsigned mask = 0;
+      int n0 = tb;
+      while (n0 < end_node) {
+        mask |= 1u << (n0 - tb);
+        const int lim = off[base + n0] + short_max;
+        int n1 = n0 + 1;
+        while (n1 < end_node && off[base + n1 + 1] <= lim) ++n1;
+        n0 = n1;
+      }
+      short_masks.push_back(mask);
+    }
     tb = -1;
     t_edges = 0;
   };
@@ -155,6 +180,8 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   s.items.insert(s.items.end(), leaves.begin(), leaves.end());
   s.items.insert(s.items.end(), longs.begin(), longs.end());
   s.items.insert(s.items.end(), shorts.begin(), shorts.end());
+  s.masks.assign(leaves.size() + longs.size(), 0u);
+  s.masks.insert(s.masks.end(), short_masks.begin(), short_masks.end());
 }
 
 struct LayerDesc {
@@ -199,6 +226,7 @@ struct KlayPlan {
   int* d_toff = nullptr;
   int* d_tpar = nullptr;
   int4* d_items = nullptr;
+  unsigned* d_masks = nullptr;
   int4* d_heavy = nullptr;
   int* d_root_node = nullptr;
   signed char* d_const = nullptr;
@@ -219,6 +247,7 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_toff);
   cudaFree(p->d_tpar);
   cudaFree(p->d_items);
+  cudaFree(p->d_masks);
   cudaFree(p->d_heavy);
   cudaFree(p->d_root_node);
   cudaFree(p->d_const);
@@ -257,6 +286,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
 
   std::vector<int> off, src, toff, tpar;
   std::vector<int4> items, heavy;
+  std::vector<unsigned> masks;  // parallel to items
   // the tail: longest suffix of layers with <= TAIL_EDGES edges
   int32_t tail_from = num_layers;
   while (tail_from > 0 && num_layers - tail_from < TAIL_MAX_LAYERS &&
@@ -329,6 +359,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
+    masks.insert(masks.end(), fs.masks.begin(), fs.masks.end());
     d.fq_base = d.fi_base;
     d.fq_n = d.fi_n;
     if (d.prod && !fs.heavy.empty()) {
@@ -337,10 +368,12 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       d.fq_base = (int64_t)items.size();
       d.fq_n = (int64_t)qs.items.size();
       items.insert(items.end(), qs.items.begin(), qs.items.end());
+      masks.insert(masks.end(), qs.masks.begin(), qs.masks.end());
     }
     d.bi_base = (int64_t)items.size();
     d.bi_n = (int64_t)bs.items.size();
     items.insert(items.end(), bs.items.begin(), bs.items.end());
+    masks.insert(masks.end(), bs.masks.begin(), bs.masks.end());
     d.fh_base = (int64_t)heavy.size();
     d.fh_n = (int64_t)fs.heavy.size();
     heavy.insert(heavy.end(), fs.heavy.begin(), fs.heavy.end());
@@ -382,7 +415,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   int rc;
   if ((rc = upload(&p->d_off, off)) || (rc = upload(&p->d_src, src)) ||
       (rc = upload(&p->d_toff, toff)) || (rc = upload(&p->d_tpar, tpar)) ||
-      (rc = upload(&p->d_items, items)) || (rc = upload(&p->d_heavy, heavy)) ||
+      (rc = upload(&p->d_items, items)) || (rc = upload(&p->d_masks, masks)) ||
+      (rc = upload(&p->d_heavy, heavy)) ||
       (rc = upload(&p->d_root_node, rn)) || (rc = upload(&p->d_const, cv)) ||
       (rc = upload(&p->d_top_off, top_off)) || (rc = upload(&p->d_top_pos, top_pos))) {
     plan_free(p);
@@ -431,6 +465,7 @@ template <typename T>
 LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, int64_t ld) {
   LayerArgs<T> a{};
   a.items = p->d_items + (fwd ? d.fi_base : d.bi_base);
+  a.masks = p->d_masks + (fwd ? d.fi_base : d.bi_base);
   a.n_items = (int)(fwd ? d.fi_n : d.bi_n);
   a.heavy = p->d_heavy + (fwd ? d.fh_base : d.bh_base);
   a.n_heavy = (int)(fwd ? d.fh_n : d.bh_n);
@@ -462,6 +497,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   if (tail_from < p->L) {
     tail = new TailArgs<T>();
     tail->n = 0;
+    tail->debug_skip = g_tail_debug ? 1 : 0;
   }
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
@@ -470,6 +506,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     if (d.prod && (sr == SR_REAL_ || sr == KLAY_MAXPROD)) {
       // sequential product: heavy segments stay whole (no leaves, no combine)
       a.items = p->d_items + d.fq_base;
+      a.masks = p->d_masks + d.fq_base;
       a.n_items = (int)d.fq_n;
       a.n_heavy = 0;
     }
@@ -487,8 +524,22 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     prev = cur;
   }
   if (tail) {
+    const LayerDesc& d0 = p->layers[tail_from];
+    const LayerDesc& dl = p->layers[p->L - 1];
+    tail->pf_ptr[0] = p->d_src + d0.e_base;
+    tail->pf_bytes[0] = (dl.e_base + dl.E - d0.e_base) * (long long)sizeof(int);
+    tail->pf_ptr[1] = p->d_off + d0.off_base;
+    tail->pf_bytes[1] = (dl.off_base + dl.W + 1 - d0.off_base) * (long long)sizeof(int);
+    tail->pf_ptr[2] = p->d_items + d0.fi_base;
+    tail->pf_bytes[2] = (dl.bi_base - d0.fi_base) * (long long)sizeof(int4);
+    tail->pf_ptr[3] = p->d_masks + d0.fi_base;
+    tail->pf_bytes[3] = (dl.bi_base - d0.fi_base) * (long long)sizeof(unsigned);
     LaunchScope ls(s, 4, tail_from + 1);
-    const int n = launch_forward_tail(sr, *tail, chunks, TAIL_CLUSTER, s);
+    int n = launch_forward_tail(sr, *tail, chunks, TAIL_CLUSTER, s);
+    if (n == 0 && TAIL_CLUSTER > 8) {  // non-portable cluster size refused: portable size
+      cudaGetLastError();
+      n = launch_forward_tail(sr, *tail, chunks, 8, s);
+    }
     delete tail;
     if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
                                             cudaGetErrorString(cudaGetLastError()));
@@ -523,6 +574,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   if (tail_from < p->L) {
     tail = new TailArgs<T>();
     tail->n = 0;
+    tail->debug_skip = g_tail_debug ? 1 : 0;
   }
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
@@ -535,8 +587,22 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     if (l >= tail_from) {
       tail->layer[tail->n++] = a;
       if (l == tail_from) {
+        const LayerDesc& d0 = p->layers[tail_from];
+        const LayerDesc& dl = p->layers[p->L - 1];
+        tail->pf_ptr[0] = p->d_tpar + d0.e_base;
+        tail->pf_bytes[0] = (dl.e_base + dl.E - d0.e_base) * (long long)sizeof(int);
+        tail->pf_ptr[1] = p->d_toff + d0.toff_base;
+        tail->pf_bytes[1] = (dl.toff_base + dl.Wprev + 1 - d0.toff_base) * (long long)sizeof(int);
+        tail->pf_ptr[2] = p->d_items + d0.bi_base;
+        tail->pf_bytes[2] = (dl.bi_base + dl.bi_n - d0.bi_base) * (long long)sizeof(int4);
+        tail->pf_ptr[3] = p->d_masks + d0.bi_base;
+        tail->pf_bytes[3] = (dl.bi_base + dl.bi_n - d0.bi_base) * (long long)sizeof(unsigned);
         LaunchScope ls(s, 5, tail_from + 1);
-        const int n = launch_backward_tail(domain, *tail, chunks, TAIL_CLUSTER, s);
+        int n = launch_backward_tail(domain, *tail, chunks, TAIL_CLUSTER, s);
+        if (n == 0 && TAIL_CLUSTER > 8) {
+          cudaGetLastError();
+          n = launch_backward_tail(domain, *tail, chunks, 8, s);
+        }
         delete tail;
         tail = nullptr;
         if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +

@@ -9,6 +9,7 @@ namespace klay {
 template <typename T>
 struct LayerArgs {
   const int4* items;  // work items of this layer/direction
+  const unsigned* masks;  // per item: stage-batch start nodes (short tasks)
   int n_items;
   const int4* heavy;  // {node, first leaf slot, #leaves, 0}
   int n_heavy;
@@ -38,6 +39,11 @@ template <typename T>
 struct TailArgs {
   LayerArgs<T> layer[TAIL_MAX_LAYERS];
   int n;
+  // plan-data ranges of all tail layers (indices, offsets, items, masks), pulled
+  // into L2 at kernel start so no layer waits on DRAM for its structure
+  const void* pf_ptr[4];
+  long long pf_bytes[4];
+  int debug_skip;  // KLAY_TAIL_DEBUG=1: barriers only (timing experiments; wrong results)
 };
 
 // forward layer: semiring x layer op -> reduction kind (RK_*)

@@ -145,9 +145,10 @@ struct ItemsSmem {
   static constexpr int EV = G::NOP * 32;           // Vec<T> per staged edge
   static constexpr int XV = G::NX * 32;            // Vec<T> per staged own value
   static constexpr int STAGE_V = SE * (EV + XV);   // Vec<T> per stage
-  static constexpr int IDX_INTS = TASK_EDGES + 32 + 33;  // widx | woff | wbat
+  static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * sizeof(Vec<T>);
+  // + one ItemIndex (sizeof = 32 + 4 * (TASK_EDGES + 32) bytes)
   static constexpr size_t warp_bytes =
-      ((size_t)2 * STAGE_V * sizeof(Vec<T>) + (size_t)IDX_INTS * sizeof(int) + 127) / 128 * 128;
+      (stage_bytes + 32 + (size_t)4 * (TASK_EDGES + 32) + 127) / 128 * 128;
   static constexpr size_t bytes = warp_bytes * WARPS_PER_BLOCK;
 };
 
@@ -171,17 +172,61 @@ __device__ __forceinline__ Vec<T> combine8(const Vec<T> (&r)[8]) {
   return res;
 }
 
-// One work item for one 512-byte column chunk, processed by one warp with
-// its own slice `wbase` of shared memory (ItemsSmem::warp_bytes).
+// ---- per-item index data (warp-private shared memory) ----------------------
+// The structure of an item (descriptor, batch mask, edge indices, segment
+// offsets) does not depend on values: the tail kernel loads it for the next
+// layer while the cluster barrier of the current layer is still open.
+struct ItemIndex {
+  int4 it;            // item descriptor (see items_kernel)
+  unsigned mask;      // short task: bit j set when node j starts a stage batch
+  int pad[3];
+  int widx[TASK_EDGES];
+  int woff[32];       // short task: segment offsets relative to it.z
+};
+
+// registers of one lane while an ItemIndex is in flight
+struct ItemRegs {
+  int4 it;
+  unsigned mask;
+  int idx[TASK_EDGES / 32];
+  int off;
+};
+
+template <typename T>
+__device__ __forceinline__ ItemRegs load_item_regs(const LayerArgs<T>& a, int item, int lane) {
+  ItemRegs r;
+  r.it = __ldg(a.items + item);
+  r.mask = __ldg(a.masks + item);
+  const int ne = r.it.w - r.it.z;
+#pragma unroll
+  for (int q = 0; q < TASK_EDGES / 32; ++q) {
+    const int e = q * 32 + lane;
+    r.idx[q] = (ne <= TASK_EDGES && e < ne) ? __ldg(a.idx + r.it.z + e) : 0;
+  }
+  const int nn = r.it.y - r.it.x;
+  r.off = (r.it.y > 0 && lane <= nn) ? __ldg(a.off + r.it.x + lane) - r.it.z : 0;
+  return r;
+}
+
+__device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r, int lane) {
+  if (lane == 0) {
+    ib->it = r.it;
+    ib->mask = r.mask;
+  }
+#pragma unroll
+  for (int q = 0; q < TASK_EDGES / 32; ++q) ib->widx[q * 32 + lane] = r.idx[q];
+  ib->woff[lane] = r.off;
+}
+
+// Run one item (index data in `ib`, synchronized) for one 512-byte column
+// chunk; `stage` is the warp's double-buffered staging area.
 template <typename T, int RK, typename G>
-__device__ __forceinline__ void process_item(const LayerArgs<T>& a, int item, int chunk,
-                                             unsigned char* wbase, int lane) {
+__device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex* ib, int chunk,
+                                         Vec<T>* stage, int lane) {
   using S = ItemsSmem<T, G>;
   constexpr int SE = S::SE, EV = S::EV, XV = S::XV, STAGE_V = S::STAGE_V;
-  Vec<T>* stage = reinterpret_cast<Vec<T>*>(wbase);
-  int* widx = reinterpret_cast<int*>(wbase + (size_t)2 * STAGE_V * sizeof(Vec<T>));
-  int* woff = widx + TASK_EDGES;
-  int* wbat = woff + 32;
+  const int* widx = ib->widx;
+  const int* woff = ib->woff;
 
   // Lanes past the row (v >= V) work on column 0 and never store: the whole
   // warp runs the same instruction stream without divergence.
@@ -189,46 +234,34 @@ __device__ __forceinline__ void process_item(const LayerArgs<T>& a, int item, in
   const bool active = v < a.V;
   const size_t col = (size_t)(active ? v : 0) * Vec<T>::N;
   const long long ld = a.ld;
-  const int4 it = __ldg(a.items + item);
+  const int4 it = ib->it;
   const int ne = it.w - it.z;
   const G g(a, col);
   const bool staged_idx = ne <= TASK_EDGES;
-  // a warp may run several items back to back (tail kernel): every lane must
-  // be done with the previous item's shared index arrays before they change
-  __syncwarp();
-  if (staged_idx)
-    for (int q = lane; q < ne; q += 32) widx[q] = __ldg(a.idx + it.z + q);
 
   if (it.y > 0) {
     // ======================= short task =======================
-    // nodes [nb, nb+nn), every segment <= SE edges; node-aligned batches of
-    // <= SE edges are staged two at a time and reduced node by node
+    // nodes [nb, nb+nn), every segment <= SE edges; the node-aligned stage
+    // batches (<= SE edges, host-computed bit mask) are staged two at a time
+    // and reduced node by node
     const int nb = it.x, nn = it.y - it.x;
-    if (lane <= nn) woff[lane] = __ldg(a.off + nb + lane) - it.z;
-    __syncwarp();
-    int nbat = 0;
-    if (lane == 0) {
-      int n0 = 0;
-      wbat[0] = 0;
-      while (n0 < nn) {
-        const int lim = woff[n0] + SE;
-        int n1 = n0 + 1;
-        while (n1 < nn && woff[n1 + 1] <= lim) ++n1;
-        wbat[++nbat] = n1;
-        n0 = n1;
-      }
-    }
-    nbat = __shfl_sync(0xffffffffu, nbat, 0);
-    __syncwarp();
+    unsigned m_issue = ib->mask, m_scan = ib->mask;
+    auto next_batch = [&](unsigned& m, int& n0, int& n1) {
+      n0 = __ffs(m) - 1;
+      m &= m - 1;
+      n1 = m ? __ffs(m) - 1 : nn;
+    };
     auto issue = [&](int b) {
       Vec<T>* st = stage + (b & 1) * STAGE_V;
-      const int n0 = wbat[b], n1 = wbat[b + 1];
+      int n0, n1;
+      next_batch(m_issue, n0, n1);
       const int eb = woff[n0], cnt = woff[n1] - eb;
       for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, widx[eb + i], lane);
       if constexpr (G::NX)
         for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nb + nd, lane);
       cp_async_commit();
     };
+    const int nbat = __popc(ib->mask);
     T* outp = a.out + (size_t)nb * ld + col;
     issue(0);
     for (int b = 0; b < nbat; ++b) {
@@ -239,7 +272,8 @@ __device__ __forceinline__ void process_item(const LayerArgs<T>& a, int item, in
         cp_async_wait<0>();
       }
       const Vec<T>* st = stage + (b & 1) * STAGE_V;
-      const int n0 = wbat[b], n1 = wbat[b + 1];
+      int n0, n1;
+      next_batch(m_scan, n0, n1);
       const int eb = woff[n0];
       for (int nd = n0; nd < n1; ++nd) {
         const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
@@ -273,7 +307,6 @@ __device__ __forceinline__ void process_item(const LayerArgs<T>& a, int item, in
   }
 
   // ===================== long segment / leaf =====================
-  __syncwarp();
   const bool leaf = it.y < 0;
   const int node = it.x;
   const int t0 = leaf ? 0 : 1;      // first tail edge (relative)
@@ -363,10 +396,15 @@ __device__ __forceinline__ void process_item(const LayerArgs<T>& a, int item, in
 template <typename T, int RK, typename G>
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  using S = ItemsSmem<T, G>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
   if (item >= a.n_items) return;  // no block-wide barriers inside
-  process_item<T, RK, G>(a, item, blockIdx.y, smem + (size_t)warp * ItemsSmem<T, G>::warp_bytes, lane);
+  unsigned char* wbase = smem + (size_t)warp * S::warp_bytes;
+  ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + S::stage_bytes);
+  store_item_regs(ib, load_item_regs(a, item, lane), lane);
+  __syncwarp();
+  run_item<T, RK, G>(a, ib, blockIdx.y, reinterpret_cast<Vec<T>*>(wbase), lane);
 }
 
 // ---- heavy-segment combine: x0 (+) leaf partials in order ---------------------
@@ -465,6 +503,13 @@ struct TailSmem {
   static constexpr size_t bytes = warp_bytes * TAIL_WARPS;
 };
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 template <typename T, int RKP, int RKS, typename GP, typename GS>
 __global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_constant__ TailArgs<T> t) {
   namespace cg = cooperative_groups;
@@ -475,26 +520,49 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_c
   const int chunk = blockIdx.x / csize;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbase = smem + (size_t)warp * TailSmem<T, GP, GS>::warp_bytes;
+  Vec<T>* stage = reinterpret_cast<Vec<T>*>(wbase);
+  constexpr size_t stage_bytes = ItemsSmem<T, GP>::stage_bytes > ItemsSmem<T, GS>::stage_bytes
+                                     ? ItemsSmem<T, GP>::stage_bytes
+                                     : ItemsSmem<T, GS>::stage_bytes;
+  ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + stage_bytes);
   const int w = rank * TAIL_WARPS + warp, cw = csize * TAIL_WARPS;
+  {
+    // pull every tail layer's structure into L2 up front
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long gthreads = (long long)gridDim.x * blockDim.x;
+    for (int r = 0; r < 4; ++r) {
+      const char* base = static_cast<const char*>(t.pf_ptr[r]);
+      for (long long o = gtid * 128; o < t.pf_bytes[r]; o += gthreads * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
+    }
+  }
+  // the first item of every layer is fetched one layer ahead, while the
+  // cluster barrier of the previous layer is still open
+  ItemRegs next;
+  if (t.n > 0 && w < t.layer[0].n_items) next = load_item_regs(t.layer[0], w, lane);
   for (int i = 0; i < t.n; ++i) {
     const LayerArgs<T>& a = t.layer[i];
     const int v = chunk * 32 + lane;
-    if (a.prod) {
-      for (int it = w; it < a.n_items; it += cw) process_item<T, RKP, GP>(a, it, chunk, wbase, lane);
-      if (a.n_heavy > 0) {
-        cluster.sync();
-        for (int h = w; h < a.n_heavy; h += cw)
-          if (v < a.V) process_heavy<T, RKP, GP>(a, h, v);
+    if (!t.debug_skip) {
+      for (int it = w; it < a.n_items; it += cw) {
+        __syncwarp();  // previous item done with ib
+        store_item_regs(ib, it == w ? next : load_item_regs(a, it, lane), lane);
+        __syncwarp();
+        if (a.prod) run_item<T, RKP, GP>(a, ib, chunk, stage, lane);
+        else run_item<T, RKS, GS>(a, ib, chunk, stage, lane);
       }
-    } else {
-      for (int it = w; it < a.n_items; it += cw) process_item<T, RKS, GS>(a, it, chunk, wbase, lane);
       if (a.n_heavy > 0) {
         cluster.sync();
         for (int h = w; h < a.n_heavy; h += cw)
-          if (v < a.V) process_heavy<T, RKS, GS>(a, h, v);
+          if (v < a.V) {
+            if (a.prod) process_heavy<T, RKP, GP>(a, h, v);
+            else process_heavy<T, RKS, GS>(a, h, v);
+          }
       }
     }
-    cluster.sync();
+    cluster_arrive();
+    if (i + 1 < t.n && w < t.layer[i + 1].n_items) next = load_item_regs(t.layer[i + 1], w, lane);
+    cluster_wait();
   }
 }
 
