@@ -11,12 +11,12 @@ int launch_backward_layer(int mode, const LayerArgs<float>& a, cudaStream_t s) {
   }
 }
 
-int launch_backward_tail(int domain, const TailArgs<float>& t, int chunks, int cluster, cudaStream_t s) {
+int launch_backward_tail(int domain, const TailArgs<float>& t, int cluster, cudaStream_t s) {
   using PASS = BwdGather<float, BW_PASS>;
   if (domain == SR_LOG)  // log: products pass through, sums weight by softmax
-    return launch_tail<float, RK_SUM, RK_SUM, PASS, BwdGather<float, BW_LOGSUM>>(t, chunks, cluster, s);
+    return launch_tail<float, RK_SUM, RK_SUM, PASS, BwdGather<float, BW_LOGSUM>>(t, cluster, s);
   // real: zero-safe product adjoint, sums pass through
-  return launch_tail<float, RK_SUM, RK_SUM, BwdGather<float, BW_REALPROD>, PASS>(t, chunks, cluster, s);
+  return launch_tail<float, RK_SUM, RK_SUM, BwdGather<float, BW_REALPROD>, PASS>(t, cluster, s);
 }
 
 }  // namespace klay

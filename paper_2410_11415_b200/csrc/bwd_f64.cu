@@ -11,12 +11,12 @@ int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s) 
   }
 }
 
-int launch_backward_tail(int domain, const TailArgs<double>& t, int chunks, int cluster, cudaStream_t s) {
+int launch_backward_tail(int domain, const TailArgs<double>& t, int cluster, cudaStream_t s) {
   using PASS = BwdGather<double, BW_PASS>;
   if (domain == SR_LOG)  // log: products pass through, sums weight by softmax
-    return launch_tail<double, RK_SUM, RK_SUM, PASS, BwdGather<double, BW_LOGSUM>>(t, chunks, cluster, s);
+    return launch_tail<double, RK_SUM, RK_SUM, PASS, BwdGather<double, BW_LOGSUM>>(t, cluster, s);
   // real: zero-safe product adjoint, sums pass through
-  return launch_tail<double, RK_SUM, RK_SUM, BwdGather<double, BW_REALPROD>, PASS>(t, chunks, cluster, s);
+  return launch_tail<double, RK_SUM, RK_SUM, BwdGather<double, BW_REALPROD>, PASS>(t, cluster, s);
 }
 
 }  // namespace klay

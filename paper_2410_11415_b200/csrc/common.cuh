@@ -26,31 +26,57 @@ enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4 };
 // numpy's pairwise summation works on blocks of at most this many elements
 constexpr int PW_BLOCK = 128;
 
+#ifndef KLAY_NV
+#define KLAY_NV 1
+#endif
+// Each lane owns NV 16-byte pieces of a row: piece q of lane l in column
+// chunk c is the row's 16-byte vector (c * NV + q) * 32 + l, so every load /
+// store instruction of a warp moves one contiguous 512-byte span and a warp
+// covers NV * 512 bytes of the row (per-edge bookkeeping amortized NV-fold).
+constexpr int NV = KLAY_NV;
+
 template <typename T>
 struct alignas(16) Vec {
-  static constexpr int N = 16 / sizeof(T);
+  static constexpr int N = NV * 16 / sizeof(T);
   T v[N];
 };
+template <typename T>
+constexpr int PIECE = 16 / (int)sizeof(T);  // elements per 16-byte piece
+template <typename T>
+constexpr int PSTRIDE = 32 * PIECE<T>;      // elements between a lane's pieces
 
-// Value loads go through L2 (ld.global.cg), never the non-coherent path:
-// the persistent tail kernel reads rows written earlier in the same launch.
-__device__ __forceinline__ Vec<float> ldv(const float* p) {
-  float4 u = __ldcg(reinterpret_cast<const float4*>(p));
+// `p` points at the lane's piece 0; pieces >= nl (past the row) repeat the
+// last valid piece, so loads never leave the row.
+__device__ __forceinline__ Vec<float> ldv(const float* p, int nl) {
   Vec<float> r;
-  r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const float4 u = __ldcg(reinterpret_cast<const float4*>(p + (q < nl ? q : nl - 1) * PSTRIDE<float>));
+    r.v[4 * q] = u.x; r.v[4 * q + 1] = u.y; r.v[4 * q + 2] = u.z; r.v[4 * q + 3] = u.w;
+  }
   return r;
 }
-__device__ __forceinline__ Vec<double> ldv(const double* p) {
-  double2 u = __ldcg(reinterpret_cast<const double2*>(p));
+__device__ __forceinline__ Vec<double> ldv(const double* p, int nl) {
   Vec<double> r;
-  r.v[0] = u.x; r.v[1] = u.y;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double2 u = __ldcg(reinterpret_cast<const double2*>(p + (q < nl ? q : nl - 1) * PSTRIDE<double>));
+    r.v[2 * q] = u.x; r.v[2 * q + 1] = u.y;
+  }
   return r;
 }
-__device__ __forceinline__ void stv(float* p, const Vec<float>& r) {
-  *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+// store the first `na` pieces (the ones inside the row)
+__device__ __forceinline__ void stv(float* p, const Vec<float>& r, int na) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+    if (q < na)
+      *reinterpret_cast<float4*>(p + q * PSTRIDE<float>) =
+          make_float4(r.v[4 * q], r.v[4 * q + 1], r.v[4 * q + 2], r.v[4 * q + 3]);
 }
-__device__ __forceinline__ void stv(double* p, const Vec<double>& r) {
-  *reinterpret_cast<double2*>(p) = make_double2(r.v[0], r.v[1]);
+__device__ __forceinline__ void stv(double* p, const Vec<double>& r, int na) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+    if (q < na) *reinterpret_cast<double2*>(p + q * PSTRIDE<double>) = make_double2(r.v[2 * q], r.v[2 * q + 1]);
 }
 
 template <typename T>
@@ -223,19 +249,37 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// Staged vectors live in shared memory as NV x 32 lanes of 16-byte pieces
+// (conflict-free): piece q of lane l at slot[q * 32 + l].
+template <typename T>
+__device__ __forceinline__ void cp_async_vec(uint4* slot, int lane, const T* p, int nl) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) cp_async16(slot + q * 32 + lane, p + (q < nl ? q : nl - 1) * PSTRIDE<T>);
+}
+template <typename T>
+__device__ __forceinline__ Vec<T> lds_vec(const uint4* slot, int lane) {
+  Vec<T> r;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const uint4 u = slot[q * 32 + lane];
+    memcpy(&r.v[q * PIECE<T>], &u, 16);
+  }
+  return r;
+}
+
 // pairwise-tree combination of leaf partials stored one row apart
 // (same recursion as numpy's pairwise_sum above PW_BLOCK elements)
 template <typename T>
-__device__ Vec<T> tree_sum(const T* leaves, long long stride, int& leaf, int len) {
+__device__ Vec<T> tree_sum(const T* leaves, long long stride, int& leaf, int len, int nl) {
   if (len <= PW_BLOCK) {
-    Vec<T> v = ldv(leaves + (size_t)leaf * stride);
+    Vec<T> v = ldv(leaves + (size_t)leaf * stride, nl);
     ++leaf;
     return v;
   }
   int n2 = len / 2;
   n2 -= n2 % 8;
-  Vec<T> a = tree_sum(leaves, stride, leaf, n2);
-  Vec<T> b = tree_sum(leaves, stride, leaf, len - n2);
+  Vec<T> a = tree_sum(leaves, stride, leaf, n2, nl);
+  Vec<T> b = tree_sum(leaves, stride, leaf, len - n2, nl);
   return vadd(a, b);
 }
 

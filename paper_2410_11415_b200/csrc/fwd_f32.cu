@@ -21,13 +21,13 @@ int launch_forward_layer(int sr, bool prod, const LayerArgs<float>& a, cudaStrea
   }
 }
 
-int launch_forward_tail(int sr, const TailArgs<float>& t, int chunks, int cluster, cudaStream_t s) {
+int launch_forward_tail(int sr, const TailArgs<float>& t, int cluster, cudaStream_t s) {
   using G = FwdGather<float>;
   switch (sr) {
-    case SR_REAL: return launch_tail<float, RK_PROD, RK_SUM, G, G>(t, chunks, cluster, s);
-    case SR_LOG: return launch_tail<float, RK_SUM, RK_LSE, G, G>(t, chunks, cluster, s);
-    case SR_BOOL: return launch_tail<float, RK_MIN, RK_MAX, G, G>(t, chunks, cluster, s);
-    default: return launch_tail<float, RK_PROD, RK_MAX, G, G>(t, chunks, cluster, s);
+    case SR_REAL: return launch_tail<float, RK_PROD, RK_SUM, G, G>(t, cluster, s);
+    case SR_LOG: return launch_tail<float, RK_SUM, RK_LSE, G, G>(t, cluster, s);
+    case SR_BOOL: return launch_tail<float, RK_MIN, RK_MAX, G, G>(t, cluster, s);
+    default: return launch_tail<float, RK_PROD, RK_MAX, G, G>(t, cluster, s);
   }
 }
 

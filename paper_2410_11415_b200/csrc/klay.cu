@@ -491,7 +491,6 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     ++g_launches;
   }
   const T* prev = values;
-  const int chunks = (V + 31) / 32;
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
   TailArgs<T>* tail = nullptr;
   if (tail_from < p->L) {
@@ -535,10 +534,10 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     tail->pf_ptr[3] = p->d_masks + d0.fi_base;
     tail->pf_bytes[3] = (dl.bi_base - d0.fi_base) * (long long)sizeof(unsigned);
     LaunchScope ls(s, 4, tail_from + 1);
-    int n = launch_forward_tail(sr, *tail, chunks, TAIL_CLUSTER, s);
+    int n = launch_forward_tail(sr, *tail, TAIL_CLUSTER, s);
     if (n == 0 && TAIL_CLUSTER > 8) {  // non-portable cluster size refused: portable size
       cudaGetLastError();
-      n = launch_forward_tail(sr, *tail, chunks, 8, s);
+      n = launch_forward_tail(sr, *tail, 8, s);
     }
     delete tail;
     if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
@@ -568,7 +567,6 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     launch_seed<T>(seed, p->d_top_off, p->d_top_pos, g[cur], (int)p->WL, p->R, B, ld, s);
     ++g_launches;
   }
-  const int chunks = (V + 31) / 32;
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
   TailArgs<T>* tail = nullptr;
   if (tail_from < p->L) {
@@ -598,10 +596,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
         tail->pf_ptr[3] = p->d_masks + d0.bi_base;
         tail->pf_bytes[3] = (dl.bi_base + dl.bi_n - d0.bi_base) * (long long)sizeof(unsigned);
         LaunchScope ls(s, 5, tail_from + 1);
-        int n = launch_backward_tail(domain, *tail, chunks, TAIL_CLUSTER, s);
+        int n = launch_backward_tail(domain, *tail, TAIL_CLUSTER, s);
         if (n == 0 && TAIL_CLUSTER > 8) {
           cudaGetLastError();
-          n = launch_backward_tail(domain, *tail, chunks, 8, s);
+          n = launch_backward_tail(domain, *tail, 8, s);
         }
         delete tail;
         tail = nullptr;

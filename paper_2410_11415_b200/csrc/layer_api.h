@@ -55,10 +55,10 @@ int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s);
 
 // persistent tail: layers t.layer[0..n) in order, one cluster per column
 // chunk; returns the number of kernels launched (0 on a launch failure)
-int launch_forward_tail(int sr, const TailArgs<float>& t, int chunks, int cluster, cudaStream_t s);
-int launch_forward_tail(int sr, const TailArgs<double>& t, int chunks, int cluster, cudaStream_t s);
-int launch_backward_tail(int domain, const TailArgs<float>& t, int chunks, int cluster, cudaStream_t s);
-int launch_backward_tail(int domain, const TailArgs<double>& t, int chunks, int cluster, cudaStream_t s);
+int launch_forward_tail(int sr, const TailArgs<float>& t, int cluster, cudaStream_t s);
+int launch_forward_tail(int sr, const TailArgs<double>& t, int cluster, cudaStream_t s);
+int launch_backward_tail(int domain, const TailArgs<float>& t, int cluster, cudaStream_t s);
+int launch_backward_tail(int domain, const TailArgs<double>& t, int cluster, cudaStream_t s);
 
 // boundary kernels
 template <typename T>

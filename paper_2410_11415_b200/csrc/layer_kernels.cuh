@@ -30,16 +30,18 @@ struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8;
   const T* base;
   long long ld;
-  __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col) : base(a.prev + col), ld(a.ld) {}
-  __device__ __forceinline__ void issue(Vec<T>* slot, int row, int lane) const {
-    cp_async16(slot + lane, base + (size_t)row * ld);
+  int nl;
+  __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col, int nl_)
+      : base(a.prev + col), ld(a.ld), nl(nl_) {}
+  __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
+    cp_async_vec(slot, lane, base + (size_t)row * ld, nl);
   }
-  __device__ __forceinline__ void issue_x(Vec<T>*, int, int) const {}
-  __device__ __forceinline__ Vec<T> value(const Vec<T>* slot, int lane, int, const Vec<T>&) const {
-    return slot[lane];
+  __device__ __forceinline__ void issue_x(uint4*, int, int) const {}
+  __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int, const Vec<T>&) const {
+    return lds_vec<T>(slot, lane);
   }
   __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>&) const {
-    return ldv(base + (size_t)row * ld);
+    return ldv(base + (size_t)row * ld, nl);
   }
   __device__ __forceinline__ Vec<T> load_x(int) const { return Vec<T>{}; }
 };
@@ -55,24 +57,25 @@ struct BwdGather {
   const int* foff;
   const int* fsrc;
   long long ld;
-  __device__ __forceinline__ BwdGather(const LayerArgs<T>& a, size_t col)
+  int nl;
+  __device__ __forceinline__ BwdGather(const LayerArgs<T>& a, size_t col, int nl_)
       : gbase(a.gcur + col), nbase(a.ncur + col), xbase(a.nprev + col), foff(a.foff),
-        fsrc(a.fsrc), ld(a.ld) {}
-  __device__ __forceinline__ void issue(Vec<T>* slot, int row, int lane) const {
-    cp_async16(slot + lane, gbase + (size_t)row * ld);
-    if constexpr (NOP == 2) cp_async16(slot + 32 + lane, nbase + (size_t)row * ld);
+        fsrc(a.fsrc), ld(a.ld), nl(nl_) {}
+  __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
+    cp_async_vec(slot, lane, gbase + (size_t)row * ld, nl);
+    if constexpr (NOP == 2) cp_async_vec(slot + NV * 32, lane, nbase + (size_t)row * ld, nl);
   }
-  __device__ __forceinline__ void issue_x(Vec<T>* slot, int node, int lane) const {
-    cp_async16(slot + lane, xbase + (size_t)node * ld);
+  __device__ __forceinline__ void issue_x(uint4* slot, int node, int lane) const {
+    cp_async_vec(slot, lane, xbase + (size_t)node * ld, nl);
   }
-  __device__ __forceinline__ Vec<T> load_x(int node) const { return ldv(xbase + (size_t)node * ld); }
-  __device__ __forceinline__ Vec<T> value(const Vec<T>* slot, int lane, int row, const Vec<T>& x) const {
-    if constexpr (NOP == 2) return combine(slot[lane], slot[32 + lane], row, x);
-    else return slot[lane];
+  __device__ __forceinline__ Vec<T> load_x(int node) const { return ldv(xbase + (size_t)node * ld, nl); }
+  __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>& x) const {
+    if constexpr (NOP == 2) return combine(lds_vec<T>(slot, lane), lds_vec<T>(slot + NV * 32, lane), row, x);
+    else return lds_vec<T>(slot, lane);
   }
   __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>& x) const {
-    const Vec<T> g = ldv(gbase + (size_t)row * ld);
-    if constexpr (NOP == 2) return combine(g, ldv(nbase + (size_t)row * ld), row, x);
+    const Vec<T> g = ldv(gbase + (size_t)row * ld, nl);
+    if constexpr (NOP == 2) return combine(g, ldv(nbase + (size_t)row * ld, nl), row, x);
     else return g;
   }
   __device__ __forceinline__ Vec<T> combine(const Vec<T>& g, const Vec<T>& P, int row,
@@ -108,7 +111,7 @@ struct BwdGather {
 #pragma unroll
     for (int c = 0; c < N; ++c) { pnz[c] = T(1); zc[c] = 0; }
     for (int s = s0; s < s1; ++s) {
-      const Vec<T> y = ldv(xbase + (size_t)__ldg(fsrc + s) * ld);
+      const Vec<T> y = ldv(xbase + (size_t)__ldg(fsrc + s) * ld, nl);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         if (y.v[c] == T(0)) ++zc[c];
@@ -142,10 +145,11 @@ constexpr int TASK_NODES = 31;   // max nodes of a short task (one lane per segm
 template <typename T, typename G>
 struct ItemsSmem {
   static constexpr int SE = G::SE;                 // edges per stage batch (= max short segment)
-  static constexpr int EV = G::NOP * 32;           // Vec<T> per staged edge
-  static constexpr int XV = G::NX * 32;            // Vec<T> per staged own value
-  static constexpr int STAGE_V = SE * (EV + XV);   // Vec<T> per stage
-  static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * sizeof(Vec<T>);
+  // stage units: 16-byte pieces; a staged vector is NV x 32 lanes of pieces
+  static constexpr int EV = G::NOP * NV * 32;      // pieces per staged edge
+  static constexpr int XV = G::NX * NV * 32;       // pieces per staged own value
+  static constexpr int STAGE_V = SE * (EV + XV);   // pieces per stage
+  static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * 16;
   // + one ItemIndex (sizeof = 32 + 4 * (TASK_EDGES + 32) bytes)
   static constexpr size_t warp_bytes =
       (stage_bytes + 32 + (size_t)4 * (TASK_EDGES + 32) + 127) / 128 * 128;
@@ -220,23 +224,39 @@ __device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r
 
 // Run one item (index data in `ib`, synchronized) for one 512-byte column
 // chunk; `stage` is the warp's double-buffered staging area.
+// this lane's columns in chunk `chunk`: na pieces inside the row (stored),
+// nl = max(na, 1) loadable pieces, col = element offset of piece 0
+struct LaneCols {
+  int na, nl;
+  size_t col;
+};
+template <typename T>
+__device__ __forceinline__ LaneCols lane_cols(int V, int chunk, int lane) {
+  const int vb = chunk * 32 * NV + lane;
+  LaneCols c;
+  c.na = min(NV, max(0, (V - vb + 31) / 32));
+  c.nl = c.na > 0 ? c.na : 1;
+  c.col = (size_t)(c.na > 0 ? vb : 0) * PIECE<T>;
+  return c;
+}
+
 template <typename T, int RK, typename G>
 __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex* ib, int chunk,
-                                         Vec<T>* stage, int lane) {
+                                         uint4* stage, int lane) {
   using S = ItemsSmem<T, G>;
   constexpr int SE = S::SE, EV = S::EV, XV = S::XV, STAGE_V = S::STAGE_V;
   const int* widx = ib->widx;
   const int* woff = ib->woff;
 
-  // Lanes past the row (v >= V) work on column 0 and never store: the whole
-  // warp runs the same instruction stream without divergence.
-  const int v = chunk * 32 + lane;
-  const bool active = v < a.V;
-  const size_t col = (size_t)(active ? v : 0) * Vec<T>::N;
+  // Lanes (pieces) past the row work on valid columns and never store: the
+  // whole warp runs the same instruction stream without divergence.
+  const LaneCols lc = lane_cols<T>(a.V, chunk, lane);
+  const int na = lc.na;
+  const size_t col = lc.col;
   const long long ld = a.ld;
   const int4 it = ib->it;
   const int ne = it.w - it.z;
-  const G g(a, col);
+  const G g(a, col, lc.nl);
   const bool staged_idx = ne <= TASK_EDGES;
 
   if (it.y > 0) {
@@ -252,7 +272,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       n1 = m ? __ffs(m) - 1 : nn;
     };
     auto issue = [&](int b) {
-      Vec<T>* st = stage + (b & 1) * STAGE_V;
+      uint4* st = stage + (b & 1) * STAGE_V;
       int n0, n1;
       next_batch(m_issue, n0, n1);
       const int eb = woff[n0], cnt = woff[n1] - eb;
@@ -271,14 +291,14 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       } else {
         cp_async_wait<0>();
       }
-      const Vec<T>* st = stage + (b & 1) * STAGE_V;
+      const uint4* st = stage + (b & 1) * STAGE_V;
       int n0, n1;
       next_batch(m_scan, n0, n1);
       const int eb = woff[n0];
       for (int nd = n0; nd < n1; ++nd) {
         const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
         Vec<T> x{};
-        if constexpr (G::NX) x = st[SE * EV + (nd - n0) * XV + lane];
+        if constexpr (G::NX) x = lds_vec<T>(st + SE * EV + (nd - n0) * XV, lane);
         auto val = [&](int e) {
           return g.value(st + e * EV, lane, (G::NOP == 2) ? widx[eb + e] : 0, x);
         };
@@ -300,7 +320,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
         } else {
           for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
         }
-        if (active) stv(outp + (size_t)nd * ld, out);
+        stv(outp + (size_t)nd * ld, out, na);
       }
     }
     return;
@@ -316,7 +336,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   auto row_of = [&](int e) { return staged_idx ? widx[e] : __ldg(a.idx + it.z + e); };
   // round t stages tail elements [8t, 8t+8)
   auto issue = [&](int t) {
-    Vec<T>* st = stage + (t & 1) * STAGE_V;
+    uint4* st = stage + (t & 1) * STAGE_V;
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
     const int my_row = (lane < cnt) ? row_of(base + lane) : 0;
@@ -344,7 +364,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     } else {
       cp_async_wait<0>();
     }
-    const Vec<T>* st = stage + (t & 1) * STAGE_V;
+    const uint4* st = stage + (t & 1) * STAGE_V;
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
     auto val = [&](int i) {
@@ -373,23 +393,23 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   if constexpr (RK == RK_SUM) {
     if (m >= 8 && mainend == m) res = combine8(r);
   }
-  if (!active) return;
+  if (na == 0) return;
   if (leaf) {
     const int slot = -it.y - 1;
     if constexpr (RK == RK_LSE) {
-      stv(a.scratch + (size_t)slot * ld + col, lse.m);
-      stv(a.scratch + a.tpart + (size_t)slot * ld + col, lse.t);
+      stv(a.scratch + (size_t)slot * ld + col, lse.m, na);
+      stv(a.scratch + a.tpart + (size_t)slot * ld + col, lse.t, na);
     } else if constexpr (RK == RK_SUM) {
-      stv(a.scratch + (size_t)slot * ld + col, res);
+      stv(a.scratch + (size_t)slot * ld + col, res, na);
     } else {
-      stv(a.scratch + (size_t)slot * ld + col, acc);
+      stv(a.scratch + (size_t)slot * ld + col, acc, na);
     }
   } else {
     Vec<T> out;
     if constexpr (RK == RK_SUM) out = (m == 0) ? x0 : vadd(x0, res);
     else if constexpr (RK == RK_LSE) out = lse.result();
     else out = acc;
-    stv(a.out + (size_t)node * ld + col, out);
+    stv(a.out + (size_t)node * ld + col, out, na);
   }
 }
 
@@ -404,34 +424,37 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T
   ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + S::stage_bytes);
   store_item_regs(ib, load_item_regs(a, item, lane), lane);
   __syncwarp();
-  run_item<T, RK, G>(a, ib, blockIdx.y, reinterpret_cast<Vec<T>*>(wbase), lane);
+  run_item<T, RK, G>(a, ib, blockIdx.y, reinterpret_cast<uint4*>(wbase), lane);
 }
 
 // ---- heavy-segment combine: x0 (+) leaf partials in order ---------------------
 
 template <typename T, int RK, typename G>
-__device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int v) {
-  const size_t col = (size_t)v * Vec<T>::N;
+__device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int chunk, int lane) {
+  const LaneCols lc = lane_cols<T>(a.V, chunk, lane);
+  if (lc.na == 0) return;
+  const int nl = lc.nl;
+  const size_t col = lc.col;
   const long long ld = a.ld;
   const int4 hv = __ldg(a.heavy + h);
-  const int node = hv.x, slot0 = hv.y, nl = hv.z;
+  const int node = hv.x, slot0 = hv.y, nleaf = hv.z;
   const int s = __ldg(a.off + node);
   const int n = __ldg(a.off + node + 1) - s;
-  const G g(a, col);
+  const G g(a, col, nl);
   const Vec<T> x = g.load_x(node);
   const Vec<T> x0 = g.direct(__ldg(a.idx + s), x);
   Vec<T> res;
   if constexpr (RK == RK_SUM) {
     int leaf = slot0;
-    res = vadd(x0, tree_sum(a.scratch + col, ld, leaf, n - 1));
+    res = vadd(x0, tree_sum(a.scratch + col, ld, leaf, n - 1, nl));
   } else if constexpr (RK == RK_LSE) {
     LseOp<T> op;
     op.eps = a.eps;
     op.begin(n);
     op.push(x0);
-    for (int l = 0; l < nl; ++l) {
-      const Vec<T> pm = ldv(a.scratch + (size_t)(slot0 + l) * ld + col);
-      const Vec<T> pt = ldv(a.scratch + a.tpart + (size_t)(slot0 + l) * ld + col);
+    for (int l = 0; l < nleaf; ++l) {
+      const Vec<T> pm = ldv(a.scratch + (size_t)(slot0 + l) * ld + col, nl);
+      const Vec<T> pt = ldv(a.scratch + a.tpart + (size_t)(slot0 + l) * ld + col, nl);
 #pragma unroll
       for (int c = 0; c < Vec<T>::N; ++c) lse_merge(op.m.v[c], op.t.v[c], pm.v[c], pt.v[c]);
     }
@@ -440,23 +463,22 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
     SeqOp<T, RK> op;
     op.begin(n);
     op.push(x0);
-    for (int l = 0; l < nl; ++l) op.push(ldv(a.scratch + (size_t)(slot0 + l) * ld + col));
+    for (int l = 0; l < nleaf; ++l) op.push(ldv(a.scratch + (size_t)(slot0 + l) * ld + col, nl));
     res = op.result();
   }
-  stv(a.out + (size_t)node * ld + col, res);
+  stv(a.out + (size_t)node * ld + col, res, lc.na);
 }
 
 template <typename T, int RK, typename G>
 __global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
   const int h = blockIdx.x;
-  const int v = blockIdx.y * 32 + threadIdx.x;
-  if (h >= a.n_heavy || v >= a.V) return;
-  process_heavy<T, RK, G>(a, h, v);
+  if (h >= a.n_heavy) return;
+  process_heavy<T, RK, G>(a, h, blockIdx.y, threadIdx.x);
 }
 
 template <typename T, int RK, typename G>
 inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
-  const unsigned chunks = (unsigned)((a.V + 31) / 32);
+  const unsigned chunks = (unsigned)((a.V + 32 * NV - 1) / (32 * NV));
   int launched = 0;
   if (a.n_items > 0) {
     ++launched;
@@ -500,7 +522,10 @@ struct TailSmem {
   static constexpr size_t warp_bytes = ItemsSmem<T, GP>::warp_bytes > ItemsSmem<T, GS>::warp_bytes
                                            ? ItemsSmem<T, GP>::warp_bytes
                                            : ItemsSmem<T, GS>::warp_bytes;
-  static constexpr size_t bytes = warp_bytes * TAIL_WARPS;
+  // as many warps (<= TAIL_WARPS) as fit the 227 KB of shared memory
+  static constexpr int warps = (227 * 1024) / warp_bytes < TAIL_WARPS ? (int)((227 * 1024) / warp_bytes)
+                                                                      : TAIL_WARPS;
+  static constexpr size_t bytes = warp_bytes * warps;
 };
 
 __device__ __forceinline__ void cluster_arrive() {
@@ -511,7 +536,8 @@ __device__ __forceinline__ void cluster_wait() {
 }
 
 template <typename T, int RKP, int RKS, typename GP, typename GS>
-__global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_constant__ TailArgs<T> t) {
+__global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
+    tail_kernel(const __grid_constant__ TailArgs<T> t) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -520,12 +546,13 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_c
   const int chunk = blockIdx.x / csize;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wbase = smem + (size_t)warp * TailSmem<T, GP, GS>::warp_bytes;
-  Vec<T>* stage = reinterpret_cast<Vec<T>*>(wbase);
+  uint4* stage = reinterpret_cast<uint4*>(wbase);
   constexpr size_t stage_bytes = ItemsSmem<T, GP>::stage_bytes > ItemsSmem<T, GS>::stage_bytes
                                      ? ItemsSmem<T, GP>::stage_bytes
                                      : ItemsSmem<T, GS>::stage_bytes;
   ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + stage_bytes);
-  const int w = rank * TAIL_WARPS + warp, cw = csize * TAIL_WARPS;
+  constexpr int TW = TailSmem<T, GP, GS>::warps;
+  const int w = rank * TW + warp, cw = csize * TW;
   {
     // pull every tail layer's structure into L2 up front
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -542,7 +569,6 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_c
   if (t.n > 0 && w < t.layer[0].n_items) next = load_item_regs(t.layer[0], w, lane);
   for (int i = 0; i < t.n; ++i) {
     const LayerArgs<T>& a = t.layer[i];
-    const int v = chunk * 32 + lane;
     if (!t.debug_skip) {
       for (int it = w; it < a.n_items; it += cw) {
         __syncwarp();  // previous item done with ib
@@ -553,11 +579,10 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_c
       }
       if (a.n_heavy > 0) {
         cluster.sync();
-        for (int h = w; h < a.n_heavy; h += cw)
-          if (v < a.V) {
-            if (a.prod) process_heavy<T, RKP, GP>(a, h, v);
-            else process_heavy<T, RKS, GS>(a, h, v);
-          }
+        for (int h = w; h < a.n_heavy; h += cw) {
+          if (a.prod) process_heavy<T, RKP, GP>(a, h, chunk, lane);
+          else process_heavy<T, RKS, GS>(a, h, chunk, lane);
+        }
       }
     }
     cluster_arrive();
@@ -567,7 +592,8 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 1) tail_kernel(const __grid_c
 }
 
 template <typename T, int RKP, int RKS, typename GP, typename GS>
-inline int launch_tail(const TailArgs<T>& t, int chunks, int cluster, cudaStream_t s) {
+inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
+  const int chunks = (t.layer[0].V + 32 * NV - 1) / (32 * NV);
   auto kern = tail_kernel<T, RKP, RKS, GP, GS>;
   constexpr size_t smem = TailSmem<T, GP, GS>::bytes;
   static bool configured = false;
@@ -580,7 +606,7 @@ inline int launch_tail(const TailArgs<T>& t, int chunks, int cluster, cudaStream
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(chunks * cluster), 1, 1);
-  cfg.blockDim = dim3(TAIL_WARPS * 32, 1, 1);
+  cfg.blockDim = dim3(TailSmem<T, GP, GS>::warps * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
