@@ -347,6 +347,13 @@ def run_gpu_arm(args):
             other_ms += t
     peak, peak_kind = load_peaks()
     dom = max(per_kind, key=lambda k: per_kind[k][0])
+    dom_name = ["fwd_layer_kernel", "bwd_layer_kernel"][dom]
+    traffic = None
+    try:  # DRAM bytes of the same launches, from the committed ncu launch list
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get(dom_name)
+    except Exception:
+        pass
     dms, dbytes, dn = per_kind[dom]
     achieved = dbytes / (dms / 1e3) / 1e9
     bpe = bytes_per_eval(tc, s, B)
@@ -397,10 +404,13 @@ def run_gpu_arm(args):
                          ">> 126 MB L2",
                    "bytes_per_eval": bpe,
                    "step_roofline_frac": value / world * bpe / (peak * 1e9)},
-        "roofline": {"bound": "hbm", "kernel": ["fwd_layer_kernel", "bwd_layer_kernel"][dom],
+        "roofline": {"bound": "hbm", "kernel": dom_name,
                      "launches_per_step": dn, "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "alg_bytes_per_step": dbytes,
+                     "traffic": traffic,
+                     "traffic_scope": "DRAM read+write bytes per step of the same launches "
+                                      "(ncu launch list, profiles/traffic.json)",
                      "kernel_ms_per_step": dms,
                      "fwd_ms": per_kind[0][0], "bwd_ms": per_kind[1][0],
                      "boundary_ms": other_ms},
@@ -416,7 +426,7 @@ def run_gpu_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=1024, help="rows per GPU")

@@ -1,7 +1,7 @@
 """Summarize an ncu launch list (--metrics gpu__time_duration.sum,
 dram__bytes_read.sum,dram__bytes_write.sum --csv) per kernel name:
 launches, device time, share of the step, DRAM bytes.
-    python tools/launch_summary.py gpurun_out/launches.csv"""
+    python tools/launch_summary.py gpurun_out/launches.csv [profiles/traffic.json]"""
 import collections
 import csv
 import sys
@@ -31,6 +31,16 @@ def main(path):
         print(f"{name[:70]:70s} {len(launches[name]):>5} {t*1e3:>8.3f} {t/total_t:>6.1%} "
               f"{b/1e6:>9.1f} {b/t/1e9 if t else 0:>7.0f}")
     print(f"total {total_t*1e3:.3f} ms (serialised, cold-cache launches)")
+    if len(sys.argv) > 2:
+        # DRAM traffic per step of the per-layer kernel classes bench.py reports
+        cls = {"fwd_layer_kernel": 0.0, "bwd_layer_kernel": 0.0}
+        for name, d in per.items():
+            b = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+            if name.startswith(("items_kernel", "combine_kernel")):
+                cls["bwd_layer_kernel" if "BwdGather" in name else "fwd_layer_kernel"] += b
+        import json
+        with open(sys.argv[2], "w") as fh:
+            json.dump({"source": path, "unit": "bytes per step", **cls}, fh, indent=1)
 
 
 if __name__ == "__main__":
