@@ -41,8 +41,16 @@ from .tensorized import (
 
 __version__ = "0.1.0"
 
+
+def __getattr__(name):  # torch surface, imported lazily (torch is heavy)
+    if name in ("CircuitModule", "KlayFunction"):
+        from . import torch_module
+        return getattr(torch_module, name)
+    raise AttributeError(name)
+
 __all__ = [
-    "BOOLEAN", "MAX_PRODUCT", "REAL", "SEMIRINGS", "DevicePlan", "EvalError", "EvalTrace",
+    "BOOLEAN", "CircuitModule", "KlayFunction", "MAX_PRODUCT", "REAL", "SEMIRINGS", "DevicePlan",
+    "EvalError", "EvalTrace",
     "KlayFormatError", "Literal", "Semiring", "TensorLayer", "TensorizedCircuit",
     "WeightAssignment", "backward", "device_plan", "evaluate_semiring", "forward_log",
     "forward_real", "gradient", "load_npz", "read_klay", "save_npz", "stats",

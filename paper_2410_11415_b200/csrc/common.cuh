@@ -267,6 +267,22 @@ __device__ __forceinline__ Vec<T> lds_vec(const uint4* slot, int lane) {
   return r;
 }
 
+// pairwise-tree combination of leaf partials staged in shared memory
+// (leaf l at pieces sm[l * 32 * NV ...], lane-interleaved like the stages)
+template <typename T>
+__device__ Vec<T> tree_sum_smem(const uint4* sm, int lane, int& leaf, int len) {
+  if (len <= PW_BLOCK) {
+    Vec<T> v = lds_vec<T>(sm + (size_t)leaf * 32 * NV, lane);
+    ++leaf;
+    return v;
+  }
+  int n2 = len / 2;
+  n2 -= n2 % 8;
+  Vec<T> a = tree_sum_smem<T>(sm, lane, leaf, n2);
+  Vec<T> b = tree_sum_smem<T>(sm, lane, leaf, len - n2);
+  return vadd(a, b);
+}
+
 // pairwise-tree combination of leaf partials stored one row apart
 // (same recursion as numpy's pairwise_sum above PW_BLOCK elements)
 template <typename T>

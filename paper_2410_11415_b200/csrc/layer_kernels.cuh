@@ -429,8 +429,11 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T
 
 // ---- heavy-segment combine: x0 (+) leaf partials in order ---------------------
 
+// `sm` (sm_pieces 16-byte pieces of warp-private shared memory) stages the
+// leaf partials with one round of independent cp.async when they fit.
 template <typename T, int RK, typename G>
-__device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int chunk, int lane) {
+__device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int chunk, int lane,
+                                              uint4* sm, int sm_pieces) {
   const LaneCols lc = lane_cols<T>(a.V, chunk, lane);
   if (lc.na == 0) return;
   const int nl = lc.nl;
@@ -445,8 +448,17 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
   const Vec<T> x0 = g.direct(__ldg(a.idx + s), x);
   Vec<T> res;
   if constexpr (RK == RK_SUM) {
-    int leaf = slot0;
-    res = vadd(x0, tree_sum(a.scratch + col, ld, leaf, n - 1, nl));
+    if (nleaf * 32 * NV <= sm_pieces) {
+      for (int l = 0; l < nleaf; ++l)
+        cp_async_vec(sm + (size_t)l * 32 * NV, lane, a.scratch + (size_t)(slot0 + l) * ld + col, nl);
+      cp_async_commit();
+      cp_async_wait<0>();
+      int leaf = 0;
+      res = vadd(x0, tree_sum_smem<T>(sm, lane, leaf, n - 1));
+    } else {
+      int leaf = slot0;
+      res = vadd(x0, tree_sum(a.scratch + col, ld, leaf, n - 1, nl));
+    }
   } else if constexpr (RK == RK_LSE) {
     LseOp<T> op;
     op.eps = a.eps;
@@ -469,11 +481,15 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
   stv(a.out + (size_t)node * ld + col, res, lc.na);
 }
 
+constexpr int COMBINE_LEAVES = 64;  // leaf partials staged per combine warp
+
 template <typename T, int RK, typename G>
 __global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int h = blockIdx.x;
   if (h >= a.n_heavy) return;
-  process_heavy<T, RK, G>(a, h, blockIdx.y, threadIdx.x);
+  process_heavy<T, RK, G>(a, h, blockIdx.y, threadIdx.x, reinterpret_cast<uint4*>(smem),
+                          COMBINE_LEAVES * 32 * NV);
 }
 
 template <typename T, int RK, typename G>
@@ -500,8 +516,15 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
   }
   if (a.n_heavy > 0) {
     ++launched;
+    constexpr size_t csmem = (size_t)COMBINE_LEAVES * 32 * NV * 16;
+    static bool cconf = false;
+    if (!cconf) {
+      cudaFuncSetAttribute(combine_kernel<T, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)csmem);
+      cconf = true;
+    }
     dim3 grid((unsigned)a.n_heavy, chunks);
-    combine_kernel<T, RK, G><<<grid, 32, 0, s>>>(a);
+    combine_kernel<T, RK, G><<<grid, 32, csmem, s>>>(a);
   }
   return launched;
 }
@@ -580,8 +603,9 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
       if (a.n_heavy > 0) {
         cluster.sync();
         for (int h = w; h < a.n_heavy; h += cw) {
-          if (a.prod) process_heavy<T, RKP, GP>(a, h, chunk, lane);
-          else process_heavy<T, RKS, GS>(a, h, chunk, lane);
+          __syncwarp();
+          if (a.prod) process_heavy<T, RKP, GP>(a, h, chunk, lane, stage, (int)(stage_bytes / 16));
+          else process_heavy<T, RKS, GS>(a, h, chunk, lane, stage, (int)(stage_bytes / 16));
         }
       }
     }

@@ -60,7 +60,7 @@ def test_oracle_matches_reference_goldens_small(name):
         _check_suite(tc, gold)
 
 
-@pytest.mark.parametrize("cfg", ["A", "B", "D"])
+@pytest.mark.parametrize("cfg", ["A", "B", "D", "E"])
 def test_oracle_matches_reference_goldens_configs(cfg):
     tc, gold = load_config(cfg)
     with np.errstate(all="ignore"):
