@@ -38,12 +38,35 @@ const int TAIL_CLUSTER = [] {       // CTAs per cluster (one cluster per column 
   const char* e = getenv("KLAY_TAIL_CLUSTER");
   return (e && *e) ? atoi(e) : 8;
 }();
-constexpr int TAIL_WARPS_H = 8;     // warps per CTA (== TAIL_WARPS)
+#ifndef KLAY_TAIL_WARPS
+#define KLAY_TAIL_WARPS 8
+#endif
+constexpr int TAIL_WARPS_H = KLAY_TAIL_WARPS;  // warps per CTA (== TAIL_WARPS)
 
 const bool g_tail_debug = [] {
   const char* e = getenv("KLAY_TAIL_DEBUG");
   return e && *e && *e != '0';
 }();
+
+// KLAY_TAIL_TRACE=1: print per-layer timing of the tail kernels (debug)
+const bool g_tail_trace = [] {
+  const char* e = getenv("KLAY_TAIL_TRACE");
+  return e && *e && *e != '0';
+}();
+unsigned long long* tail_trace_buf() {
+  static unsigned long long* buf = nullptr;
+  if (!buf) cudaMalloc(&buf, sizeof(unsigned long long) * 4 * 128);
+  return buf;
+}
+void tail_trace_dump(const char* what, int n) {
+  std::vector<unsigned long long> h(4 * 128);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h.data(), tail_trace_buf(), h.size() * 8, cudaMemcpyDeviceToHost);
+  fprintf(stderr, "%s tail (%d layers): items / arrive+prefetch / wait  [us]\n", what, n);
+  for (int i = 0; i < n; ++i)
+    fprintf(stderr, "  %2d %6.2f %6.2f %6.2f\n", i, (h[4 * i + 1] - h[4 * i]) * 1e-3,
+            (h[4 * i + 2] - h[4 * i + 1]) * 1e-3, (h[4 * i + 3] - h[4 * i + 2]) * 1e-3);
+}
 
 const bool g_no_tail = [] {
   const char* e = getenv("KLAY_NO_TAIL");
@@ -497,6 +520,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     tail = new TailArgs<T>();
     tail->n = 0;
     tail->debug_skip = g_tail_debug ? 1 : 0;
+    tail->trace_ts = g_tail_trace ? tail_trace_buf() : nullptr;
   }
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
@@ -543,6 +567,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
                                             cudaGetErrorString(cudaGetLastError()));
     g_launches += n;
+    if (g_tail_trace) tail_trace_dump("forward", p->L - tail_from);
   }
   if (outputs && p->R > 0) {
     const T zero = (sr == SR_LOG_) ? T(-INFINITY) : T(0);
@@ -573,6 +598,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     tail = new TailArgs<T>();
     tail->n = 0;
     tail->debug_skip = g_tail_debug ? 1 : 0;
+    tail->trace_ts = g_tail_trace ? tail_trace_buf() : nullptr;
   }
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
@@ -606,6 +632,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
         if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
                                                 cudaGetErrorString(cudaGetLastError()));
         g_launches += n;
+        if (g_tail_trace) tail_trace_dump("backward", p->L - tail_from);
       }
     } else {
       int mode = BW_PASS_;

@@ -44,6 +44,7 @@ struct TailArgs {
   const void* pf_ptr[4];
   long long pf_bytes[4];
   int debug_skip;  // KLAY_TAIL_DEBUG=1: barriers only (timing experiments; wrong results)
+  unsigned long long* trace_ts;  // KLAY_TAIL_TRACE=1: per-layer globaltimer stamps (debug)
 };
 
 // forward layer: semiring x layer op -> reduction kind (RK_*)

@@ -196,11 +196,13 @@ struct ItemRegs {
   int off;
 };
 
+// index loads of one item whose descriptor (it, mask) is already known
 template <typename T>
-__device__ __forceinline__ ItemRegs load_item_regs(const LayerArgs<T>& a, int item, int lane) {
+__device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int4 it, unsigned mask,
+                                                   int lane) {
   ItemRegs r;
-  r.it = __ldg(a.items + item);
-  r.mask = __ldg(a.masks + item);
+  r.it = it;
+  r.mask = mask;
   const int ne = r.it.w - r.it.z;
 #pragma unroll
   for (int q = 0; q < TASK_EDGES / 32; ++q) {
@@ -210,6 +212,11 @@ __device__ __forceinline__ ItemRegs load_item_regs(const LayerArgs<T>& a, int it
   const int nn = r.it.y - r.it.x;
   r.off = (r.it.y > 0 && lane <= nn) ? __ldg(a.off + r.it.x + lane) - r.it.z : 0;
   return r;
+}
+
+template <typename T>
+__device__ __forceinline__ ItemRegs load_item_regs(const LayerArgs<T>& a, int item, int lane) {
+  return item_regs_from(a, __ldg(a.items + item), __ldg(a.masks + item), lane);
 }
 
 __device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r, int lane) {
@@ -538,13 +545,25 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
 // written by one CTA are read by the others through L2 (cp.async.cg and
 // ld.global.cg), which the barrier's release/acquire ordering makes safe.
 
-constexpr int TAIL_WARPS = 8;
+#ifndef KLAY_TAIL_WARPS
+#define KLAY_TAIL_WARPS 8
+#endif
+constexpr int TAIL_WARPS = KLAY_TAIL_WARPS;
 
+// first-item descriptor of every tail layer for one warp (loaded once)
+struct TailDesc {
+  int4 it;
+  unsigned mask;
+  int pad[3];
+};
+
+// per warp: stage sized for the larger policy, one ItemIndex, the descriptor table
 template <typename T, typename GP, typename GS>
 struct TailSmem {
-  static constexpr size_t warp_bytes = ItemsSmem<T, GP>::warp_bytes > ItemsSmem<T, GS>::warp_bytes
+  static constexpr size_t item_bytes = ItemsSmem<T, GP>::warp_bytes > ItemsSmem<T, GS>::warp_bytes
                                            ? ItemsSmem<T, GP>::warp_bytes
                                            : ItemsSmem<T, GS>::warp_bytes;
+  static constexpr size_t warp_bytes = item_bytes + sizeof(TailDesc) * TAIL_MAX_LAYERS;
   // as many warps (<= TAIL_WARPS) as fit the 227 KB of shared memory
   static constexpr int warps = (227 * 1024) / warp_bytes < TAIL_WARPS ? (int)((227 * 1024) / warp_bytes)
                                                                       : TAIL_WARPS;
@@ -576,6 +595,13 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
   ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + stage_bytes);
   constexpr int TW = TailSmem<T, GP, GS>::warps;
   const int w = rank * TW + warp, cw = csize * TW;
+  auto stamp = [&](int i, int k) {  // KLAY_TAIL_TRACE debug timestamps
+    if (t.trace_ts && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      t.trace_ts[i * 4 + k] = ns;
+    }
+  };
   {
     // pull every tail layer's structure into L2 up front
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -586,16 +612,30 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
     }
   }
-  // the first item of every layer is fetched one layer ahead, while the
-  // cluster barrier of the previous layer is still open
+  // Every layer's first item for this warp: the descriptors of all layers
+  // are loaded once (lane-parallel, one round trip) and the index data of
+  // layer i+1 is requested at the start of layer i, so no layer waits on a
+  // dependent index load after its barrier.
+  TailDesc* desc = reinterpret_cast<TailDesc*>(wbase + TailSmem<T, GP, GS>::item_bytes);
+  for (int l = lane; l < t.n; l += 32) {
+    if (w < t.layer[l].n_items) {
+      desc[l].it = __ldg(t.layer[l].items + w);
+      desc[l].mask = __ldg(t.layer[l].masks + w);
+    }
+  }
+  __syncwarp();
   ItemRegs next;
-  if (t.n > 0 && w < t.layer[0].n_items) next = load_item_regs(t.layer[0], w, lane);
+  if (t.n > 0 && w < t.layer[0].n_items) next = item_regs_from(t.layer[0], desc[0].it, desc[0].mask, lane);
   for (int i = 0; i < t.n; ++i) {
     const LayerArgs<T>& a = t.layer[i];
+    stamp(i, 0);
+    const ItemRegs cur = next;
+    if (i + 1 < t.n && w < t.layer[i + 1].n_items)
+      next = item_regs_from(t.layer[i + 1], desc[i + 1].it, desc[i + 1].mask, lane);
     if (!t.debug_skip) {
       for (int it = w; it < a.n_items; it += cw) {
         __syncwarp();  // previous item done with ib
-        store_item_regs(ib, it == w ? next : load_item_regs(a, it, lane), lane);
+        store_item_regs(ib, it == w ? cur : load_item_regs(a, it, lane), lane);
         __syncwarp();
         if (a.prod) run_item<T, RKP, GP>(a, ib, chunk, stage, lane);
         else run_item<T, RKS, GS>(a, ib, chunk, stage, lane);
@@ -609,9 +649,11 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
         }
       }
     }
+    stamp(i, 1);
     cluster_arrive();
-    if (i + 1 < t.n && w < t.layer[i + 1].n_items) next = load_item_regs(t.layer[i + 1], w, lane);
+    stamp(i, 2);
     cluster_wait();
+    stamp(i, 3);
   }
 }
 
