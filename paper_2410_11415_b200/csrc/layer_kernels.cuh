@@ -28,6 +28,7 @@ constexpr int WARPS_PER_BLOCK = 4;
 template <typename T>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8;
+  static constexpr int MINB = 6;  // resident blocks per SM (shared memory allows 6)
   const T* base;
   long long ld;
   int nl;
@@ -51,6 +52,7 @@ struct BwdGather {
   static constexpr int NOP = (MODE == BW_PASS) ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   static constexpr int SE = 8;
+  static constexpr int MINB = 1;  // (register-bound at 6 blocks: spills)
   const T* gbase;
   const T* nbase;
   const T* xbase;
@@ -83,12 +85,22 @@ struct BwdGather {
     constexpr int N = Vec<T>::N;
     Vec<T> r;
     if constexpr (MODE == BW_LOGSUM) {
-      // g[parent] * exp(child - parent); NaN/inf weights -> 0 (engine.py:346-352)
+      // g[parent] * exp(child - parent); NaN/inf weights -> 0 (engine.py:346-352).
+      // A parent equal to its child (a unary sum, epsilon 0) has weight
+      // exp(0) = 1, or 0 when both are -inf (exp(NaN) masked): no exp needed.
+      bool same = true;
 #pragma unroll
-      for (int c = 0; c < N; ++c) {
-        T w = kexp(x.v[c] - P.v[c]);
-        w = isfinite(w) ? w : T(0);
-        r.v[c] = g.v[c] * w;
+      for (int c = 0; c < N; ++c) same &= (x.v[c] == P.v[c]);
+      if (same) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) r.v[c] = (x.v[c] == T(-INFINITY)) ? g.v[c] * T(0) : g.v[c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          T w = kexp(x.v[c] - P.v[c]);
+          w = isfinite(w) ? w : T(0);
+          r.v[c] = g.v[c] * w;
+        }
       }
     } else {
       // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
@@ -318,12 +330,16 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
             out = vadd(out, acc);
           }
         } else if constexpr (RK == RK_LSE) {
-          LseOp<T> op;
-          op.eps = a.eps;
-          op.begin(n);
-          op.push(out);
-          for (int j = 1; j < n; ++j) op.push(val(sb + j));
-          out = op.result();
+          // a unary sum with epsilon 0 is an exact copy: log(exp(x - x) + 0) + x
+          // == x, and -inf stays -inf (uniform branch: no exp/log issued)
+          if (n > 1 || a.eps != T(0)) {
+            LseOp<T> op;
+            op.eps = a.eps;
+            op.begin(n);
+            op.push(out);
+            for (int j = 1; j < n; ++j) op.push(val(sb + j));
+            out = op.result();
+          }
         } else {
           for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
         }
@@ -421,7 +437,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
 }
 
 template <typename T, int RK, typename G>
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32) items_kernel(LayerArgs<T> a) {
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(LayerArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   using S = ItemsSmem<T, G>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
