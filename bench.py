@@ -236,6 +236,53 @@ def run_reference_arm(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
+    """Device-timed evals/s of another BASELINE config (inputs in HBM)."""
+    import torch
+    from paper_2410_11415_b200 import _lib, engine
+    from paper_2410_11415_b200.tensorized import load_npz
+
+    tc = load_npz(os.path.join(ROOT, "data", "circuits", f"{name}.npz"))
+    plan = engine.device_plan(tc, dev)
+    code = {"real": _lib.KLAY_REAL, "log": _lib.KLAY_LOG, "bool": _lib.KLAY_BOOL}[semiring]
+    rng = np.random.Generator(np.random.Philox(key=1))
+    if semiring == "bool":
+        w = rng.integers(0, 2, size=(B, tc.num_inputs)).astype(np.float64)
+    else:
+        w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
+        if semiring == "log":
+            w = np.log(w)
+    wd = torch.from_numpy(w.astype(dtype)).to(dev)
+    vals = plan.alloc_values(B, dtype, retain=with_backward)
+    fw = plan.forward_workspace(B, dtype)
+    work = plan.workspace(B, dtype) if with_backward else None
+
+    def step():
+        plan.forward(wd, code, dtype, retain=with_backward, values=vals, workspace=fw)
+        if with_backward:
+            plan.backward(vals, B, code, dtype, workspace=work)
+
+    for _ in range(3):
+        step()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(iters):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / iters
+    s = 8 if dtype == np.float64 else 4
+    fwd_b, bwd_b = layer_bytes(tc, s, B, semiring if semiring in ("log", "real") else "log")
+    alg = sum(fwd_b.values()) + (sum(bwd_b.values()) if with_backward else 0)
+    peak, _ = load_peaks()
+    nodes = tc.num_inputs + sum(l.width for l in tc.layers)
+    return {"nodes": nodes, "semiring": semiring, "dtype": "f64" if s == 8 else "f32", "batch": B,
+            "pass": "fwd+bwd" if with_backward else "fwd", "ms_per_batch": ms,
+            "evals_per_s": B / (ms / 1e3), "roofline_frac": alg / (ms / 1e3) / 1e9 / peak}
+
+
 def run_gpu_arm(args):
     import torch
     import torch.distributed as dist
@@ -288,12 +335,18 @@ def run_gpu_arm(args):
     grads = torch.empty((B, tc.num_inputs), dtype=torch.float32, device=dev)
     work = plan.workspace(B, dt)
     gathered = [torch.empty_like(outputs) for _ in range(world)] if world > 1 else None
+    launches_per_step = None
+
+    # the timed step replays one CUDA graph holding the whole fwd + bwd
+    # (117 kernels for config C); the instrumented step below launches them
+    # one by one on the stream to time each
+    cap = plan.capture(B, dt, _lib.KLAY_LOG, backward=True)
+    cap.weights.copy_(w_dev)
 
     def step():
-        plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
-        plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
+        cap.replay()
         if world > 1:
-            dist.all_gather(gathered, outputs)
+            dist.all_gather(gathered, cap.outputs)
 
     stream = torch.cuda.current_stream(dev)
     clocks = ClockSampler(local)
@@ -304,7 +357,13 @@ def run_gpu_arm(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    n0 = lib.klay_launch_count()
+    # kernels per step (a graph replay launches the captured kernels; count
+    # them on one stream-launched step)
+    n_a = lib.klay_launch_count()
+    plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
+    plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
+    launches_per_step = lib.klay_launch_count() - n_a
+    torch.cuda.synchronize(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -312,7 +371,7 @@ def run_gpu_arm(args):
         step()
     ev1.record(stream)
     torch.cuda.synchronize(dev)
-    launches = lib.klay_launch_count() - n0
+    launches = launches_per_step * args.steps
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -384,6 +443,17 @@ def run_gpu_arm(args):
                "d2h_bytes_per_step": int(tr.outputs.nbytes + g.nbytes),
                "api": "engine.forward_log(dtype=float32) + engine.backward, numpy in/out"}
 
+    extra = None
+    if world == 1 and not args.no_extra:
+        # the other BASELINE configs, device-timed (parity cases; not the headline)
+        extra = {
+            "A_real_f64_b1_fwd": measure_config("A", "real", np.float64, 1, False, dev),
+            "B_log_f64_b256_fwd_bwd": measure_config("B", "log", np.float64, 256, True, dev),
+            "D_bool_b4096_fwd": measure_config("D", "bool", np.float32, 4096, False, dev),
+            "D_real_f32_b4096_fwd": measure_config("D", "real", np.float32, 4096, False, dev),
+            "E_log_f64_b128_fwd_bwd": measure_config("E", "log", np.float64, 128, True, dev),
+        }
+
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -415,9 +485,12 @@ def run_gpu_arm(args):
                      "fwd_ms": per_kind[0][0], "bwd_ms": per_kind[1][0],
                      "boundary_ms": other_ms},
         "gpu_launches": int(launches),
+        "launch_mode": "CUDA graph replay of the captured fwd+bwd "
+                       f"({launches_per_step} libklay kernels per step)",
         "clocks": clk,
         "cpu_baseline": cpu_line,
         "e2e": e2e,
+        "extra_configs": extra,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -433,6 +506,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other-config measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

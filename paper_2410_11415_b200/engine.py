@@ -281,6 +281,11 @@ class DevicePlan:
         _lib.check(rc, "klay_forward")
         return outputs, values
 
+    def capture(self, batch: int, dtype, semiring: int, epsilon: float = 0.0,
+                backward: bool = True, seeded: bool = False) -> "CapturedPass":
+        """A CUDA-graph-captured forward (+ backward) over fixed buffers."""
+        return CapturedPass(self, batch, dtype, semiring, epsilon, backward, seeded)
+
     def workspace(self, batch: int, dtype):
         torch = _torch()
         ld = self.row_stride(batch, dtype)
@@ -308,6 +313,54 @@ class DevicePlan:
             self._stream())
         _lib.check(rc, "klay_backward")
         return grads
+
+
+class CapturedPass:
+    """One forward (+ backward) pass of a plan over fixed device buffers,
+    captured once in a CUDA graph and replayed (no per-layer host launches).
+
+    Write inputs into ``weights`` ([B, K]) and ``seed`` ([B, R], backward
+    only), call ``replay()``; results land in ``outputs`` ([B, R]) and
+    ``grads`` ([B, K]) on the plan's device, stream-ordered on the current
+    stream. The buffers are reused by every replay.
+    """
+
+    def __init__(self, plan: DevicePlan, batch: int, dtype, semiring: int, epsilon: float = 0.0,
+                 backward: bool = True, seeded: bool = False):
+        torch = _torch()
+        dt = _resolve_dtype(dtype)
+        tdt = torch.float64 if dt == np.float64 else torch.float32
+        if backward and semiring not in (_lib.KLAY_REAL, _lib.KLAY_LOG):
+            raise EvalError("backward is defined for the real and log semirings only")
+        self.plan, self.batch, self.dtype = plan, batch, dt
+        dev = plan.device
+        self.weights = torch.zeros((batch, plan.num_inputs), dtype=tdt, device=dev)
+        self.outputs = torch.empty((batch, plan.num_roots), dtype=tdt, device=dev)
+        self.grads = torch.empty((batch, plan.num_inputs), dtype=tdt, device=dev) if backward else None
+        self.seed = torch.ones((batch, plan.num_roots), dtype=tdt, device=dev) if seeded else None
+        self.values = plan.alloc_values(batch, dt, retain=backward)
+        self._fw = plan.forward_workspace(batch, dt)
+        self._bw = plan.workspace(batch, dt) if backward else None
+
+        def run():
+            plan.forward(self.weights, semiring, dt, retain=backward, epsilon=epsilon,
+                         values=self.values, outputs=self.outputs, workspace=self._fw)
+            if backward:
+                plan.backward(self.values, batch, semiring, dt, seed=self.seed, grads=self.grads,
+                              workspace=self._bw)
+
+        # warm up outside capture (kernel attributes, lazy module loading)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            run()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            run()
+
+    def replay(self):
+        self.graph.replay()
 
 
 def device_plan(tc, device=None) -> DevicePlan:

@@ -245,3 +245,27 @@ def test_batch_one_and_odd_batches(cuda):
         ref, rtr = oracle.forward(tc, w, "real")
         assert np.array_equal(tr.outputs, ref)
         assert np.array_equal(k.backward(tc, tr), oracle.backward(tc, rtr, "real"))
+
+
+def test_captured_graph_pass_matches_stream_path(cuda):
+    """DevicePlan.capture: the CUDA-graph replay of fwd+bwd gives the same
+    bits as the stream-launched path, replay after replay (incl. the tail)."""
+    import torch
+    from paper_2410_11415_b200 import _lib, device_plan
+    for name, loader in (("corpus_5", load_case), ("B", load_config)):
+        tc, gold = loader(name)
+        plan = device_plan(tc)
+        lw = torch.tensor(np.log(gold["w_real"]), dtype=torch.float64, device=cuda)
+        B = lw.shape[0]
+        cap = plan.capture(B, np.float64, _lib.KLAY_LOG, backward=True, seeded=True)
+        seed = torch.tensor(gold["seed"], dtype=torch.float64, device=cuda)
+        out_ref, vals = plan.forward(lw, _lib.KLAY_LOG, np.float64)
+        g_ref = plan.backward(vals, B, _lib.KLAY_LOG, np.float64, seed=seed)
+        for _ in range(2):
+            cap.weights.copy_(lw)
+            cap.seed.copy_(seed)
+            cap.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(cap.outputs, out_ref)
+            assert torch.equal(cap.grads, g_ref)
+        rel_close(cap.grads.cpu().numpy(), gold["log_grad_seed"], 1e-12, 1e-12)
