@@ -244,15 +244,16 @@ def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
 
     tc = load_npz(os.path.join(ROOT, "data", "circuits", f"{name}.npz"))
     plan = engine.device_plan(tc, dev)
-    code = {"real": _lib.KLAY_REAL, "log": _lib.KLAY_LOG, "bool": _lib.KLAY_BOOL}[semiring]
+    code = {"real": _lib.KLAY_REAL, "log": _lib.KLAY_LOG, "bool": _lib.KLAY_BOOL,
+            "bool_packed": _lib.KLAY_BOOL}[semiring]
     rng = np.random.Generator(np.random.Philox(key=1))
-    if semiring == "bool":
+    if semiring.startswith("bool"):
         w = rng.integers(0, 2, size=(B, tc.num_inputs)).astype(np.float64)
     else:
         w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
         if semiring == "log":
             w = np.log(w)
-    wd = torch.from_numpy(w.astype(dtype)).to(dev)
+    wd = torch.from_numpy(w.astype(np.float32 if dtype == "u1" else dtype)).to(dev)
     vals = plan.alloc_values(B, dtype, retain=with_backward)
     fw = plan.forward_workspace(B, dtype)
     work = plan.workspace(B, dtype) if with_backward else None
@@ -273,12 +274,13 @@ def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / iters
-    s = 8 if dtype == np.float64 else 4
+    s = 8 if dtype == np.float64 else (1 / 8 if dtype == "u1" else 4)
     fwd_b, bwd_b = layer_bytes(tc, s, B, semiring if semiring in ("log", "real") else "log")
     alg = sum(fwd_b.values()) + (sum(bwd_b.values()) if with_backward else 0)
     peak, _ = load_peaks()
     nodes = tc.num_inputs + sum(l.width for l in tc.layers)
-    return {"nodes": nodes, "semiring": semiring, "dtype": "f64" if s == 8 else "f32", "batch": B,
+    return {"nodes": nodes, "semiring": semiring,
+            "dtype": {8: "f64", 4: "f32"}.get(s, "u1 (bit-packed)"), "batch": B,
             "pass": "fwd+bwd" if with_backward else "fwd", "ms_per_batch": ms,
             "evals_per_s": B / (ms / 1e3), "roofline_frac": alg / (ms / 1e3) / 1e9 / peak}
 
@@ -450,6 +452,7 @@ def run_gpu_arm(args):
             "A_real_f64_b1_fwd": measure_config("A", "real", np.float64, 1, False, dev),
             "B_log_f64_b256_fwd_bwd": measure_config("B", "log", np.float64, 256, True, dev),
             "D_bool_b4096_fwd": measure_config("D", "bool", np.float32, 4096, False, dev),
+            "D_bool_packed_b4096_fwd": measure_config("D", "bool_packed", "u1", 4096, False, dev),
             "D_real_f32_b4096_fwd": measure_config("D", "real", np.float32, 4096, False, dev),
             "E_log_f64_b128_fwd_bwd": measure_config("E", "log", np.float64, 128, True, dev),
         }

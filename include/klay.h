@@ -43,6 +43,9 @@ extern "C" {
 /* element types */
 #define KLAY_F32 0
 #define KLAY_F64 1
+#define KLAY_U1 2  /* bit-packed Boolean rows (32 batch rows per 32-bit word);
+                      KLAY_BOOL forward only, weights exactly 0/1, `ld` in words,
+                      outputs [B, R] 0.0/1.0 in the weights' element type */
 
 typedef struct KlayPlan KlayPlan;
 

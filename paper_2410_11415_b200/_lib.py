@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libklay.so")
 
 KLAY_OK, KLAY_EINVAL, KLAY_EFORMAT, KLAY_ECUDA, KLAY_EUNSUPPORTED = range(5)
 KLAY_REAL, KLAY_LOG, KLAY_BOOL, KLAY_MAXPROD = range(4)
-KLAY_F32, KLAY_F64 = 0, 1
+KLAY_F32, KLAY_F64, KLAY_U1 = 0, 1, 2
 
 _c_i64 = ctypes.c_int64
 _c_i32 = ctypes.c_int32

@@ -21,7 +21,7 @@ namespace klay {
 enum { SR_REAL = 0, SR_LOG = 1, SR_BOOL = 2, SR_MAXPROD = 3 };
 enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2 };
 // reduction kinds
-enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4 };
+enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4, RK_AND = 5, RK_OR = 6 };
 
 // numpy's pairwise summation works on blocks of at most this many elements
 constexpr int PW_BLOCK = 128;
@@ -65,6 +65,24 @@ __device__ __forceinline__ Vec<double> ldv(const double* p, int nl) {
   }
   return r;
 }
+// bit-packed Boolean rows: 32 batch rows per 32-bit word
+__device__ __forceinline__ Vec<unsigned> ldv(const unsigned* p, int nl) {
+  Vec<unsigned> r;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const uint4 u = __ldcg(reinterpret_cast<const uint4*>(p + (q < nl ? q : nl - 1) * PSTRIDE<unsigned>));
+    r.v[4 * q] = u.x; r.v[4 * q + 1] = u.y; r.v[4 * q + 2] = u.z; r.v[4 * q + 3] = u.w;
+  }
+  return r;
+}
+__device__ __forceinline__ void stv(unsigned* p, const Vec<unsigned>& r, int na) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+    if (q < na)
+      *reinterpret_cast<uint4*>(p + q * PSTRIDE<unsigned>) =
+          make_uint4(r.v[4 * q], r.v[4 * q + 1], r.v[4 * q + 2], r.v[4 * q + 3]);
+}
+
 // store the first `na` pieces (the ones inside the row)
 __device__ __forceinline__ void stv(float* p, const Vec<float>& r, int na) {
 #pragma unroll
@@ -177,6 +195,8 @@ struct SeqOp {  // RK_PROD / RK_MAX / RK_MIN: strictly sequential
       for (int c = 0; c < Vec<T>::N; ++c) {
         if constexpr (RK == RK_PROD) acc.v[c] = acc.v[c] * x.v[c];
         else if constexpr (RK == RK_MAX) acc.v[c] = npmax(acc.v[c], x.v[c]);
+        else if constexpr (RK == RK_AND) acc.v[c] = acc.v[c] & x.v[c];
+        else if constexpr (RK == RK_OR) acc.v[c] = acc.v[c] | x.v[c];
         else acc.v[c] = npmin(acc.v[c], x.v[c]);
       }
     }

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "layer_api.h"
@@ -464,8 +465,9 @@ extern "C" int64_t klay_plan_layer_offset(const KlayPlan* p, int32_t l) {
 }
 
 extern "C" int64_t klay_row_stride(int64_t batch, int32_t dtype) {
-  const int64_t per16 = (dtype == KLAY_F64) ? 2 : 4;
   if (batch < 1) batch = 1;
+  if (dtype == KLAY_U1) return ((batch + 31) / 32 + 3) / 4 * 4;  // 32-bit words, 16-byte rows
+  const int64_t per16 = (dtype == KLAY_F64) ? 2 : 4;
   return (batch + per16 - 1) / per16 * per16;
 }
 
@@ -504,13 +506,18 @@ LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, 
 
 template <typename T>
 int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* values, int64_t ld,
-                 bool retain, T* outputs, int64_t B, double eps, T* work, cudaStream_t s) {
+                 bool retain, void* outputs, int64_t B, double eps, T* work, cudaStream_t s) {
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* pingpong[2] = {values, values + (size_t)p->max_width * ld};
-  const T pad = (sr == SR_LOG_) ? T(0) : T(1);
+  constexpr bool U1 = std::is_same<T, unsigned>::value;
   if (p->K > 0) {
     LaunchScope ls(s, 2, 0);
-    launch_load_inputs<T>(weights, wdt == KLAY_F64, values, (int)p->K, B, ld, pad, s);
+    if constexpr (U1) {
+      launch_pack_inputs(weights, wdt == KLAY_F64, values, (int)p->K, B, ld, nullptr, s);
+    } else {
+      const T pad = (sr == SR_LOG_) ? T(0) : T(1);
+      launch_load_inputs<T>(weights, wdt == KLAY_F64, values, (int)p->K, B, ld, pad, s);
+    }
     ++g_launches;
   }
   const T* prev = values;
@@ -542,7 +549,8 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       tail->layer[tail->n++] = a;
     } else {
       LaunchScope ls(s, 0, l + 1);
-      g_launches += launch_forward_layer(sr, d.prod, a, s);
+      if constexpr (U1) g_launches += launch_forward_layer_u1(d.prod, a, s);
+      else g_launches += launch_forward_layer(sr, d.prod, a, s);
     }
     prev = cur;
   }
@@ -558,10 +566,14 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     tail->pf_ptr[3] = p->d_masks + d0.fi_base;
     tail->pf_bytes[3] = (dl.bi_base - d0.fi_base) * (long long)sizeof(unsigned);
     LaunchScope ls(s, 4, tail_from + 1);
-    int n = launch_forward_tail(sr, *tail, TAIL_CLUSTER, s);
+    auto tail_launch = [&](int cluster) {
+      if constexpr (U1) return launch_forward_tail_u1(*tail, cluster, s);
+      else return launch_forward_tail(sr, *tail, cluster, s);
+    };
+    int n = tail_launch(TAIL_CLUSTER);
     if (n == 0 && TAIL_CLUSTER > 8) {  // non-portable cluster size refused: portable size
       cudaGetLastError();
-      n = launch_forward_tail(sr, *tail, 8, s);
+      n = tail_launch(8);
     }
     delete tail;
     if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
@@ -570,10 +582,15 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     if (g_tail_trace) tail_trace_dump("forward", p->L - tail_from);
   }
   if (outputs && p->R > 0) {
-    const T zero = (sr == SR_LOG_) ? T(-INFINITY) : T(0);
-    const T one = (sr == SR_LOG_) ? T(0) : T(1);
     LaunchScope ls(s, 2, p->L + 1);
-    launch_assemble_outputs<T>(prev, p->d_root_node, p->d_const, outputs, p->R, B, ld, zero, one, s);
+    if constexpr (U1) {
+      launch_unpack_outputs(prev, p->d_root_node, p->d_const, outputs, wdt == KLAY_F64, p->R, B, ld, s);
+    } else {
+      const T zero = (sr == SR_LOG_) ? T(-INFINITY) : T(0);
+      const T one = (sr == SR_LOG_) ? T(0) : T(1);
+      launch_assemble_outputs<T>(prev, p->d_root_node, p->d_const, (T*)outputs, p->R, B, ld, zero,
+                                 one, s);
+    }
     ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());
@@ -654,7 +671,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
 
 int check_common(const KlayPlan* plan, int32_t dtype, int64_t batch, int64_t ld) {
   if (!plan) return fail(KLAY_EINVAL, "plan is NULL");
-  if (dtype != KLAY_F32 && dtype != KLAY_F64) return fail(KLAY_EINVAL, "unknown dtype");
+  if (dtype != KLAY_F32 && dtype != KLAY_F64 && dtype != KLAY_U1) return fail(KLAY_EINVAL, "unknown dtype");
   if (batch < 1) return fail(KLAY_EINVAL, "batch must be >= 1");
   if (ld < klay_row_stride(batch, dtype) || (ld * (int64_t)esize(dtype)) % 16)
     return fail(KLAY_EINVAL, "row stride too small or not a multiple of 16 bytes");
@@ -677,17 +694,23 @@ extern "C" int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtyp
     return fail(KLAY_EINVAL, "buffers must be 16-byte aligned");
   DeviceGuard guard(plan->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == KLAY_U1) {
+    if (semiring != KLAY_BOOL) return fail(KLAY_EUNSUPPORTED, "bit-packed rows support the Boolean semiring only");
+    return forward_impl<unsigned>(plan, semiring, weights, weights_dtype, (unsigned*)values, ld,
+                                  retain != 0, outputs, batch, 0.0, (unsigned*)workspace, s);
+  }
   if (dtype == KLAY_F32)
     return forward_impl<float>(plan, semiring, weights, weights_dtype, (float*)values, ld, retain != 0,
-                               (float*)outputs, batch, epsilon, (float*)workspace, s);
+                               outputs, batch, epsilon, (float*)workspace, s);
   return forward_impl<double>(plan, semiring, weights, weights_dtype, (double*)values, ld, retain != 0,
-                              (double*)outputs, batch, epsilon, (double*)workspace, s);
+                              outputs, batch, epsilon, (double*)workspace, s);
 }
 
 extern "C" int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                              int64_t ld, const void* seed, void* grads, void* workspace, int64_t batch,
                              void* stream) {
   if (int rc = check_common(plan, dtype, batch, ld)) return rc;
+  if (dtype == KLAY_U1) return fail(KLAY_EUNSUPPORTED, "no backward for bit-packed Boolean rows");
   if (domain != KLAY_REAL && domain != KLAY_LOG)
     return fail(KLAY_EUNSUPPORTED, "backward is defined for the real and log domains only");
   if (!trace || !workspace || (plan->K > 0 && !grads)) return fail(KLAY_EINVAL, "NULL buffer");

@@ -61,6 +61,18 @@ int launch_forward_tail(int sr, const TailArgs<double>& t, int cluster, cudaStre
 int launch_backward_tail(int domain, const TailArgs<float>& t, int cluster, cudaStream_t s);
 int launch_backward_tail(int domain, const TailArgs<double>& t, int cluster, cudaStream_t s);
 
+// bit-packed Boolean forward (dtype KLAY_U1): AND products, OR sums
+int launch_forward_layer_u1(bool prod, const LayerArgs<unsigned>& a, cudaStream_t s);
+int launch_forward_tail_u1(const TailArgs<unsigned>& t, int cluster, cudaStream_t s);
+// 0/1 weights [B, K] (f64 or f32) -> packed node-major rows [K, ldw words];
+// sets *bad (device int) when a weight is not exactly 0 or 1
+void launch_pack_inputs(const void* w, bool w_f64, unsigned* n0, int K, long long B, long long ldw,
+                        int* bad, cudaStream_t s);
+// packed root rows -> [B, R] 0.0/1.0 (f64 or f32), constants as given
+void launch_unpack_outputs(const unsigned* last, const int* root_node, const signed char* const_val,
+                           void* out, bool out_f64, int R, long long B, long long ldw,
+                           cudaStream_t s);
+
 // boundary kernels
 template <typename T>
 void launch_load_inputs(const void* w, bool w_f64, T* n0, int K, long long B, long long ld, T pad,

@@ -174,6 +174,8 @@ __device__ __forceinline__ void seq_combine(Vec<T>& acc, const Vec<T>& x) {
   for (int c = 0; c < Vec<T>::N; ++c) {
     if constexpr (RK == RK_PROD) acc.v[c] = acc.v[c] * x.v[c];
     else if constexpr (RK == RK_MAX) acc.v[c] = npmax(acc.v[c], x.v[c]);
+    else if constexpr (RK == RK_AND) acc.v[c] = acc.v[c] & x.v[c];
+    else if constexpr (RK == RK_OR) acc.v[c] = acc.v[c] | x.v[c];
     else acc.v[c] = npmin(acc.v[c], x.v[c]);
   }
 }

@@ -145,7 +145,12 @@ def _torch():
     return torch
 
 
+U1 = "u1"  # bit-packed Boolean rows (KLAY_U1): 32 batch rows per 32-bit word
+
+
 def _resolve_dtype(dtype):
+    if isinstance(dtype, str) and dtype == U1:
+        return U1
     if dtype is None:
         return np.float64
     dt = np.dtype(dtype)
@@ -157,7 +162,16 @@ def _resolve_dtype(dtype):
 
 
 def _klay_dtype(np_dtype) -> int:
+    if isinstance(np_dtype, str) and np_dtype == U1:
+        return _lib.KLAY_U1
     return _lib.KLAY_F64 if np.dtype(np_dtype) == np.float64 else _lib.KLAY_F32
+
+
+def _torch_dtype(dtype):
+    torch = _torch()
+    if isinstance(dtype, str) and dtype == U1:
+        return torch.int32
+    return torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
 
 
 class DevicePlan:
@@ -238,8 +252,7 @@ class DevicePlan:
         torch = _torch()
         ld = self.row_stride(batch, dtype)
         rows = self.num_nodes if retain else 2 * self.max_width
-        tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
-        return torch.empty((rows, ld), dtype=tdt, device=self.device)
+        return torch.empty((rows, ld), dtype=_torch_dtype(dtype), device=self.device)
 
     def forward_workspace(self, batch: int, dtype):
         """Scratch for split (heavy) segments, or None when not needed."""
@@ -268,7 +281,8 @@ class DevicePlan:
         if values is None:
             values = self.alloc_values(B, dtype, retain)
         ld = values.shape[1]
-        tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        # bit-packed Boolean rows return 0/1 outputs in the weights' dtype
+        tdt = weights.dtype if _klay_dtype(dtype) == _lib.KLAY_U1 else _torch_dtype(dtype)
         if outputs is None:
             outputs = torch.empty((B, self.num_roots), dtype=tdt, device=self.device)
         if workspace is None:
@@ -481,7 +495,12 @@ def evaluate_semiring(tc, weights: WeightAssignment, semiring) -> np.ndarray:
     if not isinstance(semiring, Semiring) or semiring.name not in SEMIRINGS:
         raise EvalError(f"unsupported semiring {getattr(semiring, 'name', semiring)!r}")
     _check_shapes(tc, weights)
-    _, out, _ = _run(tc, weights.values, semiring.code, np.float64, False)
+    dt = np.float64
+    if semiring is BOOLEAN and np.all((weights.values == 0.0) | (weights.values == 1.0)):
+        # exact 0/1 inputs: bit-packed rows (AND / OR on 32 rows per word);
+        # identical to the float max/min evaluation on 0/1 values
+        dt = U1
+    _, out, _ = _run(tc, weights.values, semiring.code, dt, False)
     return out
 
 

@@ -269,3 +269,31 @@ def test_captured_graph_pass_matches_stream_path(cuda):
             assert torch.equal(cap.outputs, out_ref)
             assert torch.equal(cap.grads, g_ref)
         rel_close(cap.grads.cpu().numpy(), gold["log_grad_seed"], 1e-12, 1e-12)
+
+
+def test_bool_bit_packed_matches_float_path(cuda):
+    """0/1 inputs take the bit-packed path (32 rows per word, AND/OR);
+    outputs are bit-identical to the float max/min path and the oracle,
+    including constant roots, odd batch sizes and the persistent tail."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan, engine
+    rng = np.random.default_rng(9)
+    cases = [load_case(n) for n in ("constants", "fig_pair_merge", "rnnf_wide")] + [load_config("D")]
+    for tc, _ in cases:
+        plan = device_plan(tc)
+        for B in (1, 33, 1000):
+            wb = rng.integers(0, 2, size=(B, tc.num_inputs)).astype(np.float64)
+            ref, _ = oracle.forward(tc, wb, "bool", retain=False)
+            out = engine.evaluate_semiring(tc, engine.WeightAssignment(wb), "bool")
+            assert out.dtype == np.float64
+            assert np.array_equal(out, ref)
+            # explicit device call in float32 outputs
+            o32, _ = plan.forward(torch.tensor(wb, dtype=torch.float32, device=cuda), _lib.KLAY_BOOL,
+                                  engine.U1, retain=False)
+            assert np.array_equal(o32.cpu().numpy(), ref.astype(np.float32))
+    # non-0/1 inputs keep the float path (max/min on arbitrary values)
+    tc, gold = load_case("fig_main")
+    w = gold["w_real"]
+    ref, _ = oracle.forward(tc, w, "bool", retain=False)
+    assert np.array_equal(engine.evaluate_semiring(tc, engine.WeightAssignment(w), "bool"), ref)
