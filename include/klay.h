@@ -127,6 +127,34 @@ int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const voi
 
 size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 
+/* ---- host-side layerization ----------------------- */
+
+/*
+ * layerize() + tensorize() of one or more constant-folded circuits
+ * (laycirc/layerize.py:158-271, tensorize.py:135-194), bit-identical index
+ * vectors. Circuits are given as flat arrays (circuit c owns nodes
+ * [node_offsets[c], node_offsets[c+1]), ids local to the circuit):
+ *   kinds[n]        0 leaf, 1 and, 2 or, 3 true, 4 false
+ *   literals[n]     DIMACS literal of a leaf (0 otherwise)
+ *   child_offsets   CSR over all nodes (global), children[] = local child ids
+ *   roots           root_offsets[c]..[c+1] (local ids); num_vars[c]
+ * Read the result with klay_layered_info / _export, free with _destroy.
+ * Errors: KLAY_EFORMAT (CircuitError cases) with klay_layerize_error().
+ */
+typedef struct KlayLayered KlayLayered;
+int klay_layerize(int32_t num_circuits, const int64_t* node_offsets, const int8_t* kinds,
+                  const int32_t* literals, const int64_t* child_offsets, const int32_t* children,
+                  const int64_t* root_offsets, const int32_t* roots, const int32_t* num_vars,
+                  KlayLayered** out);
+/* 0 num_inputs, 1 num_vars, 2 gate layers, 3 total edges, 4 non-constant
+ * roots, 5 constant roots */
+int64_t klay_layered_info(const KlayLayered* layered, int32_t what);
+int klay_layered_export(const KlayLayered* layered, int64_t* widths, int64_t* edge_counts,
+                        int64_t* sources, int64_t* segments, int32_t* input_lits,
+                        int64_t* root_indices, int64_t* const_pos, int8_t* const_val);
+void klay_layered_destroy(KlayLayered* layered);
+const char* klay_layerize_error(void);
+
 /* ---- instrumentation (no counterpart in the reference) ---------------- */
 
 /* Number of kernels this library has launched so far (process-wide). */

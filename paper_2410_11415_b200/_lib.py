@@ -37,6 +37,12 @@ SIGNATURES = {
     "klay_forward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
     "klay_backward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _vp, _vp, _vp, _c_i64, _vp]),
     "klay_backward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
+    "klay_layerize": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     ctypes.POINTER(_vp)]),
+    "klay_layered_info": (_c_i64, [_vp, _c_i32]),
+    "klay_layered_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "klay_layered_destroy": (None, [_vp]),
+    "klay_layerize_error": (ctypes.c_char_p, []),
     "klay_launch_count": (_c_i64, []),
     "klay_profiler_begin": (ctypes.c_int, []),
     "klay_profiler_end": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp]),
