@@ -24,6 +24,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define KLAY_API __attribute__((visibility("default")))
+#else
+#define KLAY_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -50,10 +56,10 @@ extern "C" {
 typedef struct KlayPlan KlayPlan;
 
 /* Library version string. */
-const char* klay_version(void);
+KLAY_API const char* klay_version(void);
 
 /* Thread-local message for the last nonzero return code of this thread. */
-const char* klay_last_error(void);
+KLAY_API const char* klay_last_error(void);
 
 /*
  * Build the immutable device plan of a tensorized circuit and upload it to
@@ -72,22 +78,22 @@ const char* klay_last_error(void);
  * The structural invariants of tensorize.py:94-132 are re-checked on the
  * host; a violation returns KLAY_EFORMAT.
  */
-int klay_plan_create(int64_t num_inputs, int32_t num_layers, const int64_t* widths,
+KLAY_API int klay_plan_create(int64_t num_inputs, int32_t num_layers, const int64_t* widths,
                      const int64_t* edge_counts, const int64_t* sources,
                      const int64_t* segments, int32_t num_roots, const int64_t* root_nodes,
                      const int8_t* const_vals, int32_t device, KlayPlan** out);
 
-int klay_plan_destroy(KlayPlan* plan);
+KLAY_API int klay_plan_destroy(KlayPlan* plan);
 
 /* Sum of all layer widths including the K input rows (= trace rows). */
-int64_t klay_plan_num_nodes(const KlayPlan* plan);
+KLAY_API int64_t klay_plan_num_nodes(const KlayPlan* plan);
 /* Largest row count of any single layer (inputs included). */
-int64_t klay_plan_max_width(const KlayPlan* plan);
+KLAY_API int64_t klay_plan_max_width(const KlayPlan* plan);
 /* Row offset of layer l (0 = inputs) inside the trace buffer. */
-int64_t klay_plan_layer_offset(const KlayPlan* plan, int32_t layer);
+KLAY_API int64_t klay_plan_layer_offset(const KlayPlan* plan, int32_t layer);
 
 /* Smallest legal row stride (elements) for batch B and element type. */
-int64_t klay_row_stride(int64_t batch, int32_t dtype);
+KLAY_API int64_t klay_row_stride(int64_t batch, int32_t dtype);
 
 /*
  * Forward pass. Replaces forward_real / forward_log / evaluate_semiring
@@ -103,14 +109,14 @@ int64_t klay_row_stride(int64_t batch, int32_t dtype);
  *   workspace    device scratch of klay_forward_workspace() bytes (may be
  *                NULL when that is 0: no segment needs a split reduction)
  */
-int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
+KLAY_API int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
                  const void* weights, int32_t weights_dtype, void* values, int64_t ld,
                  int32_t retain, void* outputs, int64_t batch, double epsilon,
                  void* workspace, void* stream);
 
 /* Scratch bytes klay_forward needs for row stride `ld` (leaf partials of
  * segments longer than 129 edges, split in numpy pairwise-tree order). */
-size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
+KLAY_API size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 
 /*
  * Backward pass over a retained trace. Replaces engine.backward
@@ -121,11 +127,11 @@ size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
  *   grads        device [B, K] row-major in `dtype`
  *   workspace    device scratch of klay_backward_workspace() bytes
  */
-int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
+KLAY_API int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                   int64_t ld, const void* seed, void* grads, void* workspace,
                   int64_t batch, void* stream);
 
-size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
+KLAY_API size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 
 /* ---- host-side layerization ----------------------- */
 
@@ -142,23 +148,23 @@ size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
  * Errors: KLAY_EFORMAT (CircuitError cases) with klay_layerize_error().
  */
 typedef struct KlayLayered KlayLayered;
-int klay_layerize(int32_t num_circuits, const int64_t* node_offsets, const int8_t* kinds,
+KLAY_API int klay_layerize(int32_t num_circuits, const int64_t* node_offsets, const int8_t* kinds,
                   const int32_t* literals, const int64_t* child_offsets, const int32_t* children,
                   const int64_t* root_offsets, const int32_t* roots, const int32_t* num_vars,
                   KlayLayered** out);
 /* 0 num_inputs, 1 num_vars, 2 gate layers, 3 total edges, 4 non-constant
  * roots, 5 constant roots */
-int64_t klay_layered_info(const KlayLayered* layered, int32_t what);
-int klay_layered_export(const KlayLayered* layered, int64_t* widths, int64_t* edge_counts,
+KLAY_API int64_t klay_layered_info(const KlayLayered* layered, int32_t what);
+KLAY_API int klay_layered_export(const KlayLayered* layered, int64_t* widths, int64_t* edge_counts,
                         int64_t* sources, int64_t* segments, int32_t* input_lits,
                         int64_t* root_indices, int64_t* const_pos, int8_t* const_val);
-void klay_layered_destroy(KlayLayered* layered);
-const char* klay_layerize_error(void);
+KLAY_API void klay_layered_destroy(KlayLayered* layered);
+KLAY_API const char* klay_layerize_error(void);
 
 /* ---- instrumentation (no counterpart in the reference) ---------------- */
 
 /* Number of kernels this library has launched so far (process-wide). */
-int64_t klay_launch_count(void);
+KLAY_API int64_t klay_launch_count(void);
 
 /* Time every subsequent launch of this thread with CUDA events on its
  * stream until klay_profiler_end (which synchronizes). Record kinds:
@@ -166,8 +172,8 @@ int64_t klay_launch_count(void);
  * boundary (inputs / outputs), 3 = backward boundary (seeds / grads),
  * 4 / 5 = forward / backward persistent tail (all layers >= `layers`);
  * `layers` holds the 1-based gate layer (0 / L+1 for boundary kernels). */
-int klay_profiler_begin(void);
-int klay_profiler_end(int32_t max_records, int32_t* kinds, int32_t* layers, float* ms,
+KLAY_API int klay_profiler_begin(void);
+KLAY_API int klay_profiler_end(int32_t max_records, int32_t* kinds, int32_t* layers, float* ms,
                       int32_t* n_records);
 
 #ifdef __cplusplus
