@@ -19,7 +19,7 @@ CIRCUITS = os.path.join(ROOT, "data", "circuits")
 
 SMALL_CASES = sorted(
     f[:-4] for f in os.listdir(os.path.join(GOLDEN, "circuits")) if f.endswith(".npz"))
-CONFIGS = ["A", "B", "C", "D", "E"]
+CONFIGS = ["A", "B", "C", "D", "E", "Cp"]
 
 # The reference CLI commands that produced each committed consumer dump
 # (/root/reference/pkg/scripts/make_consumer_fixtures.py:54-70):

@@ -67,8 +67,9 @@ def test_oracle_matches_reference_goldens_configs(cfg):
         _check_suite(tc, gold)
 
 
-def test_oracle_matches_reference_goldens_config_c_log():
-    tc, gold = load_config("C")
+@pytest.mark.parametrize("cfg", ["C", "Cp"])
+def test_oracle_matches_reference_goldens_config_c_log(cfg):
+    tc, gold = load_config(cfg)
     w = gold["w_real"]
     with np.errstate(divide="ignore"):
         lw = np.log(w)

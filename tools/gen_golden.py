@@ -132,7 +132,7 @@ def main(argv):
             w, wb, seed = weights_for(tc, rng, 6)
             np.savez_compressed(os.path.join(GOLD, f"{name}.npz"), **run_reference(tc, w, wb, seed))
             print("golden", name, tc.num_inputs, [l.width for l in tc.layers], flush=True)
-    for cfg in ("A", "B", "C", "D", "E"):
+    for cfg in ("A", "B", "C", "D", "E", "Cp"):
         if argv and cfg not in argv:
             continue
         path = os.path.join(ROOT, "data", "circuits", f"{cfg}.npz")
