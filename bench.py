@@ -455,6 +455,7 @@ def run_gpu_arm(args):
             "D_bool_packed_b4096_fwd": measure_config("D", "bool_packed", "u1", 4096, False, dev),
             "D_real_f32_b4096_fwd": measure_config("D", "real", np.float32, 4096, False, dev),
             "E_log_f64_b128_fwd_bwd": measure_config("E", "log", np.float64, 128, True, dev),
+            "Cp_log_f32_b1024_fwd_bwd": measure_config("Cp", "log", np.float32, 1024, True, dev, iters=5),
         }
 
     if world > 1:

@@ -17,6 +17,9 @@
 namespace klay {
 
 constexpr int WARPS_PER_BLOCK = 4;
+#ifndef KLAY_PASS_MINB
+#define KLAY_PASS_MINB 5  // resident blocks of the pass-through backward kernel
+#endif
 
 
 // ---- operand policies -------------------------------------------------------
@@ -52,7 +55,7 @@ struct BwdGather {
   static constexpr int NOP = (MODE == BW_PASS) ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   static constexpr int SE = 8;
-  static constexpr int MINB = 1;  // (register-bound at 6 blocks: spills)
+  static constexpr int MINB = (NOP == 1) ? KLAY_PASS_MINB : 1;  // (6 blocks: spills)
   const T* gbase;
   const T* nbase;
   const T* xbase;
