@@ -18,6 +18,7 @@ from .engine import (
     Semiring,
     WeightAssignment,
     backward,
+    clear_cache,
     device_plan,
     evaluate_semiring,
     forward_log,
@@ -52,7 +53,7 @@ __all__ = [
     "BOOLEAN", "CircuitModule", "KlayFunction", "MAX_PRODUCT", "REAL", "SEMIRINGS", "DevicePlan",
     "EvalError", "EvalTrace",
     "KlayFormatError", "Literal", "Semiring", "TensorLayer", "TensorizedCircuit",
-    "WeightAssignment", "backward", "device_plan", "evaluate_semiring", "forward_log",
+    "WeightAssignment", "backward", "clear_cache", "device_plan", "evaluate_semiring", "forward_log",
     "forward_real", "gradient", "load_npz", "read_klay", "save_npz", "stats",
     "weights_from_json", "weights_from_map", "weights_from_probabilities", "write_klay",
 ]

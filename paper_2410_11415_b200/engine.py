@@ -544,11 +544,57 @@ def backward(tc, trace: EvalTrace, seed: np.ndarray | None = None) -> np.ndarray
     return grads.cpu().numpy()
 
 
+_PASS_CACHE: dict = {}
+
+
+def clear_cache() -> None:
+    """Drop the cached captured passes of ``gradient`` (frees their buffers)."""
+    _PASS_CACHE.clear()
+
+
 def gradient(tc, weights: WeightAssignment, log_domain: bool = False, epsilon: float = 0.0,
-             seed: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
-    """Forward + backward; returns (outputs, input grads) (engine.py:372-384)."""
-    if log_domain:
-        trace = forward_log(tc, weights.to_log(), epsilon=epsilon)
-    else:
-        trace = forward_real(tc, weights)
-    return trace.outputs, backward(tc, trace, seed)
+             seed: np.ndarray | None = None, dtype=None) -> tuple[np.ndarray, np.ndarray]:
+    """Forward + backward; returns (outputs, input grads) (engine.py:372-384).
+
+    No trace escapes this call, so it runs a CUDA-graph-captured pass cached
+    per (circuit, batch, dtype, domain, epsilon, seeded): one H2D copy of the
+    weights (and seed), one graph replay, one D2H copy of outputs and grads.
+    ``dtype`` (float64 default, or float32) is an extension of the reference
+    signature; ``clear_cache()`` frees the cached buffers."""
+    torch = _torch()
+    w = weights.to_log() if log_domain else weights
+    if log_domain and epsilon < 0:
+        raise EvalError("epsilon must be >= 0")
+    if not log_domain and w.domain != REAL_DOMAIN:
+        raise EvalError("forward_real requires real-domain weights")
+    _check_shapes(tc, w)
+    dt = _resolve_dtype(dtype)
+    if dt == U1:
+        raise EvalError("gradient needs a float dtype")
+    plan = device_plan(tc)
+    B = w.batch
+    code = _lib.KLAY_LOG if log_domain else _lib.KLAY_REAL
+    key = (id(plan), B, np.dtype(dt).str, code, float(epsilon), seed is not None)
+    cap = _PASS_CACHE.get(key)
+    if cap is None or cap.plan is not plan:
+        cap = plan.capture(B, dt, code, epsilon=epsilon, backward=True, seeded=seed is not None)
+        tdt = cap.weights.dtype
+        cap.h_weights = torch.empty(cap.weights.shape, dtype=tdt, pin_memory=True)
+        cap.h_out = torch.empty(cap.outputs.shape, dtype=tdt, pin_memory=True)
+        cap.h_grad = torch.empty(cap.grads.shape, dtype=tdt, pin_memory=True)
+        if seed is not None:
+            cap.h_seed = torch.empty(cap.seed.shape, dtype=tdt, pin_memory=True)
+        _PASS_CACHE[key] = cap
+    cap.h_weights.numpy()[...] = w.values
+    cap.weights.copy_(cap.h_weights, non_blocking=True)
+    if seed is not None:
+        sd = np.asarray(seed, dtype=np.dtype(dt))
+        if sd.shape != (B, tc.num_roots):
+            raise EvalError(f"seed must have shape {(B, tc.num_roots)}")
+        cap.h_seed.numpy()[...] = sd
+        cap.seed.copy_(cap.h_seed, non_blocking=True)
+    cap.replay()
+    cap.h_out.copy_(cap.outputs, non_blocking=True)
+    cap.h_grad.copy_(cap.grads, non_blocking=True)
+    torch.cuda.current_stream(plan.device).synchronize()
+    return cap.h_out.numpy().copy(), cap.h_grad.numpy().copy()

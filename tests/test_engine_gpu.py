@@ -297,3 +297,25 @@ def test_bool_bit_packed_matches_float_path(cuda):
     w = gold["w_real"]
     ref, _ = oracle.forward(tc, w, "bool", retain=False)
     assert np.array_equal(engine.evaluate_semiring(tc, engine.WeightAssignment(w), "bool"), ref)
+
+
+def test_gradient_captured_pass_matches_trace_path(cuda):
+    """engine.gradient (cached CUDA-graph pass) == forward + backward, and
+    repeated calls with new weights / seeds do not leak state."""
+    k = _engine()
+    for name in ("constants", "corpus_5"):
+        tc, gold = load_case(name)
+        W = k.WeightAssignment(gold["w_real"])
+        for log_domain in (True, False):
+            for seed in (None, gold["seed"]):
+                for dt in (np.float64, np.float32):
+                    out, g = k.gradient(tc, W, log_domain=log_domain, seed=seed, dtype=dt)
+                    tr = (k.forward_log(tc, W.to_log(), dtype=dt) if log_domain
+                          else k.forward_real(tc, W, dtype=dt))
+                    assert np.array_equal(out, tr.outputs)
+                    assert np.array_equal(g, k.backward(tc, tr, seed))
+        W2 = k.WeightAssignment(gold["w_real"][::-1].copy())
+        out2, g2 = k.gradient(tc, W2, log_domain=True)
+        tr = k.forward_log(tc, W2.to_log())
+        assert np.array_equal(out2, tr.outputs) and np.array_equal(g2, k.backward(tc, tr))
+    k.clear_cache()
