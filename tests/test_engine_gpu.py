@@ -319,3 +319,27 @@ def test_gradient_captured_pass_matches_trace_path(cuda):
         tr = k.forward_log(tc, W2.to_log())
         assert np.array_equal(out2, tr.outputs) and np.array_equal(g2, k.backward(tc, tr))
     k.clear_cache()
+
+
+def test_config_c_large_batch_4096(cuda):
+    """B = 4096 fp32 (16.6 GB trace): 64-bit row addressing, 32 column
+    chunks; golden rows embedded at both ends of the batch."""
+    import torch
+    from paper_2410_11415_b200 import _lib, device_plan
+    tc, gold = load_config("C")
+    plan = device_plan(tc)
+    B = 4096
+    rng = np.random.Generator(np.random.Philox(key=4))
+    w = np.log(rng.uniform(0.05, 0.95, size=(B, tc.num_inputs)))
+    lw = np.log(gold["w_real"])
+    w[:8] = lw
+    w[-8:] = lw
+    wd = torch.from_numpy(w.astype(np.float32)).to(cuda)
+    out, vals = plan.forward(wd, _lib.KLAY_LOG, np.float32)
+    g = plan.backward(vals, B, _lib.KLAY_LOG, np.float32)
+    out, g = out.cpu().numpy(), g.cpu().numpy()
+    for sl in (slice(0, 8), slice(B - 8, B)):
+        rel_close(out[sl], gold["log_out"], 1e-5)
+        rel_close(g[sl], gold["log_grad"], 1e-5, 1e-5)
+    del vals
+    torch.cuda.empty_cache()
