@@ -55,16 +55,23 @@ def load_peaks():
 def layer_bytes(tc, s, B, domain="log"):
     """Per-launch algorithmic bytes of every forward and backward layer kernel.
     fwd_l = s*B*(W_{l-1}+W_l) + 4*(E_l+W_l+1);
-    bwd_l = c_l*s*B*(W_{l-1}+W_l) + 4*(2E_l+W_{l-1}+1), c_l = 2 for log-sum
-    (and real-product) layers, 1 for pass-through layers."""
+    bwd_l = s*B*(2*W_{l-1} + W_l + P_l) + 4*(2E_l+W_{l-1}+1): parent
+    gradients (W_l rows) in, child values (W_{l-1}) in, child gradients
+    (W_{l-1}) out, plus P_l parent values: 0 for pass-through layers, W_l for
+    real-product layers, and for log-sum layers (epsilon 0) only the parents
+    with fan-in > 1 -- a unary parent's value is its child's own."""
     fwd, bwd = {}, {}
     prev = tc.num_inputs
     for l, layer in enumerate(tc.layers, start=1):
         W, E = layer.width, len(layer.sources)
-        heavy = (layer.op != "prod") if domain == "log" else (layer.op == "prod")
-        c = 2 if heavy else 1
         fwd[l] = s * B * (prev + W) + 4 * (E + W + 1)
-        bwd[l] = c * s * B * (prev + W) + 4 * (2 * E + prev + 1)
+        if domain == "log" and layer.op != "prod":
+            P = int((np.bincount(np.asarray(layer.segments), minlength=W) > 1).sum())
+            bwd[l] = s * B * (2 * prev + W + P) + 4 * (2 * E + prev + 1)
+        elif domain != "log" and layer.op == "prod":
+            bwd[l] = 2 * s * B * (prev + W) + 4 * (2 * E + prev + 1)
+        else:
+            bwd[l] = s * B * (prev + W) + 4 * (2 * E + prev + 1)
         prev = W
     return fwd, bwd
 

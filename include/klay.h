@@ -126,10 +126,15 @@ KLAY_API size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int6
  *   seed         device [B, R] row-major in `dtype`, or NULL for all-ones
  *   grads        device [B, K] row-major in `dtype`
  *   workspace    device scratch of klay_backward_workspace() bytes
+ *   epsilon      the epsilon the (log-domain) trace was computed with
+ *                (the reference keeps it in trace.epsilon). Exactly 0 lets
+ *                unary sum parents skip their value reads (their weight
+ *                exp(child - parent) is then exactly 1, or 0 at -inf); any
+ *                other value, e.g. -1 when unknown, reads every parent.
  */
 KLAY_API int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                   int64_t ld, const void* seed, void* grads, void* workspace,
-                  int64_t batch, void* stream);
+                  int64_t batch, double epsilon, void* stream);
 
 KLAY_API size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 

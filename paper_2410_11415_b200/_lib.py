@@ -35,7 +35,8 @@ SIGNATURES = {
     "klay_forward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i32, _vp, _c_i64, _c_i32, _vp,
                                     _c_i64, ctypes.c_double, _vp, _vp]),
     "klay_forward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
-    "klay_backward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _vp, _vp, _vp, _c_i64, _vp]),
+    "klay_backward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _vp, _vp, _vp, _c_i64,
+                                      ctypes.c_double, _vp]),
     "klay_backward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
     "klay_layerize": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_vp)]),

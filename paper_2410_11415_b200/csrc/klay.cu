@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -370,7 +371,10 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     }
     const size_t tb = tpar.size();
     tpar.resize(tb + E);
-    for (int64_t e = 0; e < E; ++e) tpar[tb + pos[S[e]]++] = (int)G[e];
+    // bit 31 marks an edge whose parent is a unary sum: its forward value is
+    // the child's own when epsilon is 0, so the LOGSUM backward never loads it
+    for (int64_t e = 0; e < E; ++e)
+      tpar[tb + pos[S[e]]++] = (int)G[e] | ((!d.prod && cnt[G[e]] == 1) ? INT32_MIN : 0);
     // work items: forward over parents, backward over children
     ItemSet fs, bs;
     // tail layers: about one item per cluster warp (fewer, larger items)
@@ -599,7 +603,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
 
 template <typename T>
 int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, const T* seed,
-                  T* grads, T* work, int64_t B, cudaStream_t s) {
+                  T* grads, T* work, int64_t B, double epsilon, cudaStream_t s) {
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* g[2] = {work, work + (size_t)p->max_width * ld};
   T* scratch = work + (size_t)2 * p->max_width * ld;
@@ -625,6 +629,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.ncur = trace + (size_t)d.row * ld;
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
+    a.unary_ok = (domain == SR_LOG_ && epsilon == 0.0) ? 1 : 0;
     if (l >= tail_from) {
       tail->layer[tail->n++] = a;
       if (l == tail_from) {
@@ -708,7 +713,7 @@ extern "C" int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtyp
 
 extern "C" int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                              int64_t ld, const void* seed, void* grads, void* workspace, int64_t batch,
-                             void* stream) {
+                             double epsilon, void* stream) {
   if (int rc = check_common(plan, dtype, batch, ld)) return rc;
   if (dtype == KLAY_U1) return fail(KLAY_EUNSUPPORTED, "no backward for bit-packed Boolean rows");
   if (domain != KLAY_REAL && domain != KLAY_LOG)
@@ -720,9 +725,9 @@ extern "C" int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == KLAY_F32)
     return backward_impl<float>(plan, domain, (const float*)trace, ld, (const float*)seed, (float*)grads,
-                                (float*)workspace, batch, s);
+                                (float*)workspace, batch, epsilon, s);
   return backward_impl<double>(plan, domain, (const double*)trace, ld, (const double*)seed,
-                               (double*)grads, (double*)workspace, batch, s);
+                               (double*)grads, (double*)workspace, batch, epsilon, s);
 }
 
 extern "C" int64_t klay_launch_count(void) { return g_launches.load(); }

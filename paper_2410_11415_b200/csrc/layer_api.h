@@ -30,6 +30,7 @@ struct LayerArgs {
   const int* foff;    // forward CSR (real-product zero path)
   const int* fsrc;
   int prod;           // product layer (selects the reduction in the tail kernel)
+  int unary_ok;       // backward: edges flagged as unary parents need no parent value
 };
 
 // The persistent tail kernel (thin upper layers in one launch) takes its

@@ -63,25 +63,51 @@ struct BwdGather {
   const int* fsrc;
   long long ld;
   int nl;
+  bool unary_ok;
   __device__ __forceinline__ BwdGather(const LayerArgs<T>& a, size_t col, int nl_)
       : gbase(a.gcur + col), nbase(a.ncur + col), xbase(a.nprev + col), foff(a.foff),
-        fsrc(a.fsrc), ld(a.ld), nl(nl_) {}
+        fsrc(a.fsrc), ld(a.ld), nl(nl_), unary_ok(a.unary_ok != 0) {}
+  // Edge rows of the transposed CSR carry bit 31 when the parent is a unary
+  // sum (klay.cu plan build); with epsilon 0 such a parent's value equals the
+  // child's, so LOGSUM skips loading it (unary_ok) and every mode masks the bit.
+  __device__ __forceinline__ bool unary_edge(int row) const {
+    return MODE == BW_LOGSUM && unary_ok && row < 0;
+  }
   __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
-    cp_async_vec(slot, lane, gbase + (size_t)row * ld, nl);
-    if constexpr (NOP == 2) cp_async_vec(slot + NV * 32, lane, nbase + (size_t)row * ld, nl);
+    const size_t r = (size_t)(row & 0x7fffffff);
+    cp_async_vec(slot, lane, gbase + r * ld, nl);
+    if constexpr (NOP == 2)
+      if (!unary_edge(row)) cp_async_vec(slot + NV * 32, lane, nbase + r * ld, nl);
   }
   __device__ __forceinline__ void issue_x(uint4* slot, int node, int lane) const {
     cp_async_vec(slot, lane, xbase + (size_t)node * ld, nl);
   }
   __device__ __forceinline__ Vec<T> load_x(int node) const { return ldv(xbase + (size_t)node * ld, nl); }
   __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>& x) const {
-    if constexpr (NOP == 2) return combine(lds_vec<T>(slot, lane), lds_vec<T>(slot + NV * 32, lane), row, x);
-    else return lds_vec<T>(slot, lane);
+    if constexpr (NOP == 2) {
+      if (unary_edge(row)) return unary(lds_vec<T>(slot, lane), x);
+      return combine(lds_vec<T>(slot, lane), lds_vec<T>(slot + NV * 32, lane), row, x);
+    } else {
+      return lds_vec<T>(slot, lane);
+    }
   }
   __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>& x) const {
-    const Vec<T> g = ldv(gbase + (size_t)row * ld, nl);
-    if constexpr (NOP == 2) return combine(g, ldv(nbase + (size_t)row * ld, nl), row, x);
-    else return g;
+    const size_t r = (size_t)(row & 0x7fffffff);
+    const Vec<T> g = ldv(gbase + r * ld, nl);
+    if constexpr (NOP == 2) {
+      if (unary_edge(row)) return unary(g, x);
+      return combine(g, ldv(nbase + r * ld, nl), row, x);
+    } else {
+      return g;
+    }
+  }
+  // weight exp(child - parent) of a unary parent (parent == child): 1, or 0
+  // when both are -inf (exp(NaN) masked, engine.py:346-352)
+  __device__ __forceinline__ static Vec<T> unary(const Vec<T>& g, const Vec<T>& x) {
+    Vec<T> r;
+#pragma unroll
+    for (int c = 0; c < Vec<T>::N; ++c) r.v[c] = (x.v[c] == T(-INFINITY)) ? g.v[c] * T(0) : g.v[c];
+    return r;
   }
   __device__ __forceinline__ Vec<T> combine(const Vec<T>& g, const Vec<T>& P, int row,
                                             const Vec<T>& x) const {

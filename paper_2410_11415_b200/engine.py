@@ -293,6 +293,8 @@ class DevicePlan:
             outputs.data_ptr() if self.num_roots else None, B, float(epsilon),
             workspace.data_ptr() if workspace is not None else None, self._stream())
         _lib.check(rc, "klay_forward")
+        # the trace's epsilon, for backward()'s unary-parent shortcut
+        values.klay_epsilon = float(epsilon) if semiring == _lib.KLAY_LOG else -1.0
         return outputs, values
 
     def capture(self, batch: int, dtype, semiring: int, epsilon: float = 0.0,
@@ -307,9 +309,11 @@ class DevicePlan:
         return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
 
     def backward(self, values, batch: int, domain: int, dtype, seed=None, grads=None,
-                 workspace=None):
+                 workspace=None, epsilon=None):
         """values: retained trace buffer from forward(). seed: cuda [B, R] or
-        None (ones). Returns grads [B, K] tensor."""
+        None (ones). epsilon: the trace's epsilon (default: the one forward()
+        recorded on `values`; unknown disables the unary-parent shortcut).
+        Returns grads [B, K] tensor."""
         torch = _torch()
         tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
         if grads is None:
@@ -324,6 +328,7 @@ class DevicePlan:
             self._handle, domain, _klay_dtype(dtype), values.data_ptr(), values.shape[1],
             seed.data_ptr() if seed is not None else None,
             grads.data_ptr() if self.num_inputs else None, workspace.data_ptr(), batch,
+            float(epsilon if epsilon is not None else getattr(values, "klay_epsilon", -1.0)),
             self._stream())
         _lib.check(rc, "klay_backward")
         return grads
@@ -529,18 +534,21 @@ def backward(tc, trace: EvalTrace, seed: np.ndarray | None = None) -> np.ndarray
     plan = device_plan(tc)
     buf = getattr(trace, "_device_values", None)
     if buf is None or getattr(trace, "_plan", None) is not plan:
+        # a host trace may hold any values: read every parent (epsilon unknown)
         buf, dt = _upload_trace(tc, trace, plan)
         batch = trace.node_values[0].shape[0]
+        eps = -1.0
     else:
         dt = trace._dtype
         batch = trace.outputs.shape[0]
+        eps = trace.epsilon
     if seed is not None:
         seed = np.asarray(seed, dtype=dt)
         if seed.shape != (batch, tc.num_roots):
             raise EvalError(f"seed must have shape {(batch, tc.num_roots)}")
         seed = torch.from_numpy(np.ascontiguousarray(seed)).to(plan.device, non_blocking=True)
     domain = _lib.KLAY_LOG if trace.domain == LOG_DOMAIN else _lib.KLAY_REAL
-    grads = plan.backward(buf, batch, domain, dt, seed=seed)
+    grads = plan.backward(buf, batch, domain, dt, seed=seed, epsilon=eps)
     return grads.cpu().numpy()
 
 

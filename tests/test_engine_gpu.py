@@ -343,3 +343,35 @@ def test_config_c_large_batch_4096(cuda):
         rel_close(g[sl], gold["log_grad"], 1e-5, 1e-5)
     del vals
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["fig_main", "corpus_5", "rnnf_small", "B", "Cp"])
+def test_unary_parent_shortcut_is_bit_exact(cuda, name):
+    """With epsilon 0 the log-sum backward skips the values of unary parents
+    (klay.cu: bit 31 of the transposed CSR). Gradients must be bit-identical
+    to the path that reads every parent (epsilon unknown = -1), including
+    rows with -inf children (zero weights)."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan
+    tc, gold = (load_config if name in CONFIGS else load_case)(name)
+    plan = device_plan(tc)
+    w = np.array(gold["w_real"], dtype=np.float64)[:64]
+    w[::3, ::2] = 0.0  # -inf log-weights
+    with np.errstate(divide="ignore"):
+        lw = np.log(w)
+    for dt in (np.float64, np.float32):
+        x = torch.tensor(lw, dtype=torch.float64 if dt == np.float64 else torch.float32,
+                         device=cuda)
+        _, vals = plan.forward(x, _lib.KLAY_LOG, dt)
+        assert vals.klay_epsilon == 0.0
+        g_short = plan.backward(vals, x.shape[0], _lib.KLAY_LOG, dt)
+        g_full = plan.backward(vals, x.shape[0], _lib.KLAY_LOG, dt, epsilon=-1.0)
+        assert torch.equal(torch.isnan(g_short), torch.isnan(g_full))
+        assert torch.equal(torch.nan_to_num(g_short), torch.nan_to_num(g_full))
+    # with epsilon > 0 every parent is read (the reference's exp(x - P))
+    _, tr = oracle.forward(tc, lw, "log", epsilon=1e-3)
+    x = torch.tensor(lw, dtype=torch.float64, device=cuda)
+    _, vals = plan.forward(x, _lib.KLAY_LOG, np.float64, epsilon=1e-3)
+    g = plan.backward(vals, x.shape[0], _lib.KLAY_LOG, np.float64)
+    rel_close(g.cpu().numpy(), oracle.backward(tc, tr, "log"), 1e-12, 1e-12)
