@@ -162,7 +162,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   const int E = off[base + W] - off[base];
   if (cap <= 0) cap = std::max(short_max, std::min(TASK_EDGES_H, (E / 296) & ~7));
   std::vector<int4> leaves, longs, shorts;
-  std::vector<unsigned> short_masks;
+  std::vector<unsigned> short_masks, leaf_heavy;
   std::vector<std::pair<int, int>> lv;
   int tb = -1, t_edges = 0;
   auto flush = [&](int end_node) {
@@ -190,7 +190,10 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
       lv.clear();
       split_leaves(s0 + 1, n - 1, lv);
       s.heavy.push_back(make_int4(p, s.slots, (int)lv.size(), 0));
-      for (auto& l : lv) leaves.push_back(make_int4(p, -(s.slots++) - 1, l.first, l.second));
+      for (auto& l : lv) {
+        leaves.push_back(make_int4(p, -(s.slots++) - 1, l.first, l.second));
+        leaf_heavy.push_back((unsigned)(s.heavy.size() - 1));  // a leaf's mask: its heavy segment
+      }
     } else if (n > short_max) {
       flush(p);
       longs.push_back(make_int4(p, 0, s0, s0 + n));
@@ -205,7 +208,8 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   s.items.insert(s.items.end(), leaves.begin(), leaves.end());
   s.items.insert(s.items.end(), longs.begin(), longs.end());
   s.items.insert(s.items.end(), shorts.begin(), shorts.end());
-  s.masks.assign(leaves.size() + longs.size(), 0u);
+  s.masks = leaf_heavy;
+  s.masks.resize(leaves.size() + longs.size(), 0u);
   s.masks.insert(s.masks.end(), short_masks.begin(), short_masks.end());
 }
 
@@ -244,6 +248,7 @@ struct KlayPlan {
   int64_t total_rows = 0;
   int64_t max_width = 0;
   int64_t max_fslots = 0, max_bslots = 0;
+  int64_t max_heavy = 0;  // heavy segments of the largest layer (leaf counters)
   std::vector<LayerDesc> layers;
   std::vector<int64_t> layer_row;  // L+1 entries
   int* d_off = nullptr;
@@ -404,6 +409,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     masks.insert(masks.end(), bs.masks.begin(), bs.masks.end());
     d.fh_base = (int64_t)heavy.size();
     d.fh_n = (int64_t)fs.heavy.size();
+    p->max_heavy = std::max<int64_t>(p->max_heavy, std::max(fs.heavy.size(), bs.heavy.size()));
     heavy.insert(heavy.end(), fs.heavy.begin(), fs.heavy.end());
     d.bh_base = (int64_t)heavy.size();
     d.bh_n = (int64_t)bs.heavy.size();
@@ -477,15 +483,22 @@ extern "C" int64_t klay_row_stride(int64_t batch, int32_t dtype) {
 
 static size_t esize(int32_t dtype) { return dtype == KLAY_F64 ? 8 : 4; }
 
+// one int per (heavy segment, 512-byte column chunk) of a layer
+static size_t counter_bytes(const KlayPlan* p, int32_t dtype, int64_t ld) {
+  const int64_t chunks = (ld * (int64_t)esize(dtype) / 16 + 31) / 32;
+  return ((size_t)p->max_heavy * chunks * sizeof(int) + 15) / 16 * 16;
+}
+
 extern "C" size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
-  if (!plan) return 0;
-  // heavy-segment leaf partials; LSE keeps (max, sum) pairs
-  return (size_t)2 * plan->max_fslots * ld * esize(dtype);
+  if (!plan || plan->max_fslots == 0) return 0;
+  // heavy-segment leaf partials (LSE keeps (max, sum) pairs) + leaf counters
+  return (size_t)2 * plan->max_fslots * ld * esize(dtype) + counter_bytes(plan, dtype, ld);
 }
 
 extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
   if (!plan) return 0;
-  return ((size_t)2 * plan->max_width + plan->max_bslots) * ld * esize(dtype);
+  return ((size_t)2 * plan->max_width + plan->max_bslots) * ld * esize(dtype) +
+         counter_bytes(plan, dtype, ld);
 }
 
 namespace {
@@ -525,6 +538,11 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     ++g_launches;
   }
   const T* prev = values;
+  int* hcount = nullptr;
+  if (p->max_fslots > 0) {
+    hcount = reinterpret_cast<int*>(work + (size_t)2 * p->max_fslots * ld);
+    KLAY_CUDA(cudaMemsetAsync(hcount, 0, counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld), s));
+  }
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
   TailArgs<T>* tail = nullptr;
   if (tail_from < p->L) {
@@ -552,6 +570,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     if (l >= tail_from) {
       tail->layer[tail->n++] = a;
     } else {
+      a.hcount = hcount;
       LaunchScope ls(s, 0, l + 1);
       if constexpr (U1) g_launches += launch_forward_layer_u1(d.prod, a, s);
       else g_launches += launch_forward_layer(sr, d.prod, a, s);
@@ -607,6 +626,11 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* g[2] = {work, work + (size_t)p->max_width * ld};
   T* scratch = work + (size_t)2 * p->max_width * ld;
+  int* hcount = reinterpret_cast<int*>(scratch + (size_t)p->max_bslots * ld);
+  if (p->max_heavy > 0) {
+    const size_t nb = counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld);
+    KLAY_CUDA(cudaMemsetAsync(hcount, 0, nb, s));
+  }
   int cur = 0;
   {
     LaunchScope ls(s, 3, p->L + 1);
@@ -630,6 +654,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
     a.unary_ok = (domain == SR_LOG_ && epsilon == 0.0) ? 1 : 0;
+    a.hcount = (l >= tail_from) ? nullptr : hcount;
     if (l >= tail_from) {
       tail->layer[tail->n++] = a;
       if (l == tail_from) {

@@ -31,6 +31,8 @@ struct LayerArgs {
   const int* fsrc;
   int prod;           // product layer (selects the reduction in the tail kernel)
   int unary_ok;       // backward: edges flagged as unary parents need no parent value
+  int* hcount;        // per (heavy segment, chunk) leaf counters: the last leaf combines
+                      // (null: a separate combine pass / the tail's own barrier)
 };
 
 // The persistent tail kernel (thin upper layers in one launch) takes its

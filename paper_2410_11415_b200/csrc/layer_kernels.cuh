@@ -291,6 +291,10 @@ __device__ __forceinline__ LaneCols lane_cols(int V, int chunk, int lane) {
 }
 
 template <typename T, int RK, typename G>
+__device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int chunk, int lane,
+                                              uint4* sm, int sm_pieces);
+
+template <typename T, int RK, typename G>
 __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex* ib, int chunk,
                                          uint4* stage, int lane) {
   using S = ItemsSmem<T, G>;
@@ -447,8 +451,8 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   if constexpr (RK == RK_SUM) {
     if (m >= 8 && mainend == m) res = combine8(r);
   }
-  if (na == 0) return;
   if (leaf) {
+    // (stores of lanes past the row are empty: na == 0)
     const int slot = -it.y - 1;
     if constexpr (RK == RK_LSE) {
       stv(a.scratch + (size_t)slot * ld + col, lse.m, na);
@@ -458,7 +462,25 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     } else {
       stv(a.scratch + (size_t)slot * ld + col, acc, na);
     }
+    if (a.hcount) {
+      // the warp that writes the last leaf partial of (segment, chunk)
+      // finishes the segment in tree order (threadfence reduction: partials
+      // published before the count, read back through L2 after it)
+      const int h = (int)ib->mask;
+      __threadfence();
+      __syncwarp();
+      int* cnt = a.hcount + (size_t)h * gridDim.y + chunk;
+      int last = 0;
+      if (lane == 0) last = atomicAdd(cnt, 1) == __ldg(&a.heavy[h].z) - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        process_heavy<T, RK, G>(a, h, chunk, lane, stage, 2 * STAGE_V);
+        if (lane == 0) *cnt = 0;  // ready for the next layer / pass
+      }
+    }
   } else {
+    if (na == 0) return;
     Vec<T> out;
     if constexpr (RK == RK_SUM) out = (m == 0) ? x0 : vadd(x0, res);
     else if constexpr (RK == RK_LSE) out = lse.result();
@@ -568,7 +590,7 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
     dim3 grid((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
     items_kernel<T, RK, G><<<grid, WARPS_PER_BLOCK * 32, smem, s>>>(a);
   }
-  if (a.n_heavy > 0) {
+  if (a.n_heavy > 0 && !a.hcount) {
     ++launched;
     constexpr size_t csmem = (size_t)COMBINE_LEAVES * 32 * NV * 16;
     static bool cconf = false;
