@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "layer_api.h"
@@ -19,6 +20,9 @@ namespace klay {
 constexpr int WARPS_PER_BLOCK = 4;
 #ifndef KLAY_PASS_MINB
 #define KLAY_PASS_MINB 5  // resident blocks of the pass-through backward kernel
+#endif
+#ifndef KLAY_LOGSUM_MINB
+#define KLAY_LOGSUM_MINB 1
 #endif
 
 
@@ -55,7 +59,8 @@ struct BwdGather {
   static constexpr int NOP = (MODE == BW_PASS) ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   static constexpr int SE = 8;
-  static constexpr int MINB = (NOP == 1) ? KLAY_PASS_MINB : 1;  // (6 blocks: spills)
+  static constexpr int MINB = (NOP == 1) ? KLAY_PASS_MINB            // (6 blocks: spills)
+                              : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB : 1);
   const T* gbase;
   const T* nbase;
   const T* xbase;
@@ -475,6 +480,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
         __threadfence();
+        // (inlined: an out-of-line call here costs the whole kernel ~10%)
         process_heavy<T, RK, G>(a, h, chunk, lane, stage, 2 * STAGE_V);
         if (lane == 0) *cnt = 0;  // ready for the next layer / pass
       }
@@ -498,9 +504,26 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
   if (item >= a.n_items) return;  // no block-wide barriers inside
   unsigned char* wbase = smem + (size_t)warp * S::warp_bytes;
   ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + S::stage_bytes);
-  store_item_regs(ib, load_item_regs(a, item, lane), lane);
+  // The item's index data is plan data: load it before waiting on the
+  // previous layer's kernel (programmatic dependent launch, launch_layer),
+  // and let the next layer's blocks start their own prologue meanwhile.
+  const ItemRegs r = load_item_regs(a, item, lane);
+#ifndef KLAY_NO_GDC
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+  store_item_regs(ib, r, lane);
   __syncwarp();
   run_item<T, RK, G>(a, ib, blockIdx.y, reinterpret_cast<uint4*>(wbase), lane);
+}
+
+// KLAY_NO_PDL=1 launches layer kernels fully serialized (A/B switch)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KLAY_NO_PDL");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
 }
 
 // ---- heavy-segment combine: x0 (+) leaf partials in order ---------------------
@@ -587,8 +610,17 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
                            cudaSharedmemCarveoutMaxShared);
       configured = true;
     }
-    dim3 grid((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
-    items_kernel<T, RK, G><<<grid, WARPS_PER_BLOCK * 32, smem, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
+    cfg.blockDim = dim3(WARPS_PER_BLOCK * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, items_kernel<T, RK, G>, a);
   }
   if (a.n_heavy > 0 && !a.hcount) {
     ++launched;
