@@ -34,7 +34,7 @@ constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are spl
 // at most TAIL_EDGES edges runs in one launch per direction
 const int TAIL_EDGES = [] {
   const char* e = getenv("KLAY_TAIL_EDGES");
-  return (e && *e) ? atoi(e) : 2048;
+  return (e && *e) ? atoi(e) : 256;
 }();
 const int TAIL_CLUSTER = [] {       // CTAs per cluster (one cluster per column chunk)
   const char* e = getenv("KLAY_TAIL_CLUSTER");

@@ -727,6 +727,13 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
   __syncwarp();
   ItemRegs next;
   if (t.n > 0 && w < t.layer[0].n_items) next = item_regs_from(t.layer[0], desc[0].it, desc[0].mask, lane);
+  // all of the above is plan data: wait for the previous kernel's values
+  // only now (programmatic dependent launch), and let the next kernel's
+  // blocks take the SMs the tail leaves idle for their own prologue
+#ifndef KLAY_NO_GDC
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
   for (int i = 0; i < t.n; ++i) {
     const LayerArgs<T>& a = t.layer[i];
     stamp(i, 0);
@@ -776,13 +783,15 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
   cfg.blockDim = dim3(TailSmem<T, GP, GS>::warps * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, t) == cudaSuccess ? 1 : 0;
 }
 
