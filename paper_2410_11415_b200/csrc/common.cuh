@@ -211,8 +211,15 @@ __device__ __forceinline__ void lse_merge(T& m, T& t, T m2, T t2) {
   if (m2 > m) {
     t = t * kexp(m - m2) + t2;
     m = m2;
+  } else if (isnan(m2)) {
+    m = m2;  // np.maximum.reduceat propagates NaN into the peak: the result is NaN
+    t = m2;
   } else if (m2 == -INFINITY) {
     // contributes nothing (an all -inf part is masked to 0, engine.py:279)
+  } else if (m2 == INFINITY) {
+    // m == +inf too: every shifted term is masked to 0; only a NaN input
+    // (carried as a NaN sum) must survive
+    if (isnan(t2)) t = t2;
   } else {
     t = t + t2 * kexp(m2 - m);
   }
@@ -240,7 +247,11 @@ struct LseOp {
       } else if (xv > m.v[c]) {
         t.v[c] = t.v[c] * kexp(m.v[c] - xv) + T(1);
         m.v[c] = xv;
-      } else if (xv != T(-INFINITY)) {
+      } else if (isnan(xv)) {
+        m.v[c] = xv;  // the peak (np.maximum.reduceat) propagates NaN
+        t.v[c] = xv;
+      } else if (xv != T(-INFINITY) && xv != T(INFINITY)) {
+        // (xv == +inf here means m == +inf: exp(NaN) -> 0 in the reference)
         t.v[c] = t.v[c] + kexp(xv - m.v[c]);
       }
     }
@@ -251,7 +262,10 @@ struct LseOp {
 #pragma unroll
     for (int c = 0; c < Vec<T>::N; ++c) {
       // log(1 + 0) + m == m exactly: unary segments (79% of sum nodes) skip the log
-      const T res = (t.v[c] == T(1) && eps == T(0)) ? m.v[c] : klog(t.v[c] + eps) + m.v[c];
+      T res = (t.v[c] == T(1) && eps == T(0)) ? m.v[c] : klog(t.v[c] + eps) + m.v[c];
+      // a +inf peak shifts every element to exp(NaN or -inf) -> 0 in the
+      // reference (engine.py:274-282): log(0 + eps) + inf = NaN, or +inf for eps > 0
+      if (m.v[c] == T(INFINITY) && !isnan(t.v[c])) res = (eps > T(0)) ? T(INFINITY) : T(NAN);
       r.v[c] = (m.v[c] == T(-INFINITY)) ? T(-INFINITY) : res;
     }
     return r;

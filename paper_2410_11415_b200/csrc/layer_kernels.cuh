@@ -106,12 +106,13 @@ struct BwdGather {
       return g;
     }
   }
-  // weight exp(child - parent) of a unary parent (parent == child): 1, or 0
-  // when both are -inf (exp(NaN) masked, engine.py:346-352)
+  // weight exp(child - parent) of a unary parent: exp(0) = 1 for a finite
+  // child; a -inf, +inf (parent NaN) or NaN child gives exp(NaN), masked to 0
+  // (engine.py:346-352)
   __device__ __forceinline__ static Vec<T> unary(const Vec<T>& g, const Vec<T>& x) {
     Vec<T> r;
 #pragma unroll
-    for (int c = 0; c < Vec<T>::N; ++c) r.v[c] = (x.v[c] == T(-INFINITY)) ? g.v[c] * T(0) : g.v[c];
+    for (int c = 0; c < Vec<T>::N; ++c) r.v[c] = isfinite(x.v[c]) ? g.v[c] : g.v[c] * T(0);
     return r;
   }
   __device__ __forceinline__ Vec<T> combine(const Vec<T>& g, const Vec<T>& P, int row,
@@ -126,8 +127,9 @@ struct BwdGather {
 #pragma unroll
       for (int c = 0; c < N; ++c) same &= (x.v[c] == P.v[c]);
       if (same) {
+        // (x == P excludes NaN; +-inf children give exp(NaN) -> 0)
 #pragma unroll
-        for (int c = 0; c < N; ++c) r.v[c] = (x.v[c] == T(-INFINITY)) ? g.v[c] * T(0) : g.v[c];
+        for (int c = 0; c < N; ++c) r.v[c] = isfinite(x.v[c]) ? g.v[c] : g.v[c] * T(0);
       } else {
 #pragma unroll
         for (int c = 0; c < N; ++c) {

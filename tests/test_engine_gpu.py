@@ -375,3 +375,32 @@ def test_unary_parent_shortcut_is_bit_exact(cuda, name):
     _, vals = plan.forward(x, _lib.KLAY_LOG, np.float64, epsilon=1e-3)
     g = plan.backward(vals, x.shape[0], _lib.KLAY_LOG, np.float64)
     rel_close(g.cpu().numpy(), oracle.backward(tc, tr, "log"), 1e-12, 1e-12)
+
+
+@pytest.mark.parametrize("name", ["fig_main", "corpus_5", "rnnf_small", "rnnf_wide", "B"])
+@pytest.mark.parametrize("eps", [0.0, 1e-3])
+def test_log_domain_nonfinite_inputs_match_oracle(cuda, name, eps):
+    """+inf / -inf / NaN log-weights follow the reference's masked
+    logsumexp (engine.py:274-282: a +inf peak gives NaN, or +inf with
+    epsilon > 0) and its masked backward weights (engine.py:346-352)."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan
+    tc, gold = (load_config if name in CONFIGS else load_case)(name)
+    rng = np.random.default_rng(11)
+    B = 48
+    lw = np.log(rng.uniform(0.05, 0.95, size=(B, tc.num_inputs)))
+    kinds = rng.integers(0, 8, size=lw.shape)
+    lw[kinds == 0] = np.inf
+    lw[kinds == 1] = -np.inf
+    lw[(kinds == 2) & (rng.uniform(size=lw.shape) < 0.2)] = np.nan
+    lw[: B // 4] = np.log(rng.uniform(0.05, 0.95, size=(B // 4, tc.num_inputs)))  # finite rows
+    plan = device_plan(tc)
+    with np.errstate(all="ignore"):
+        ref, tr = oracle.forward(tc, lw, "log", epsilon=eps)
+        gref = oracle.backward(tc, tr, "log")
+    x = torch.tensor(lw, dtype=torch.float64, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_LOG, np.float64, epsilon=eps)
+    g = plan.backward(vals, B, _lib.KLAY_LOG, np.float64)
+    rel_close(out.cpu().numpy(), ref, 1e-12, 1e-12)
+    rel_close(g.cpu().numpy(), gref, 1e-10, 1e-12)
