@@ -225,6 +225,15 @@ __device__ __forceinline__ void lse_merge(T& m, T& t, T m2, T t2) {
   }
 }
 
+// logsumexp of one element with epsilon 0: the element itself, except that a
+// +inf element becomes NaN (log(0) + inf, engine.py:274-282)
+template <typename T>
+__device__ __forceinline__ Vec<T> lse_unary(Vec<T> x) {
+#pragma unroll
+  for (int c = 0; c < Vec<T>::N; ++c) x.v[c] = (x.v[c] == T(INFINITY)) ? T(NAN) : x.v[c];
+  return x;
+}
+
 template <typename T>
 struct LseOp {
   Vec<T> m, t;

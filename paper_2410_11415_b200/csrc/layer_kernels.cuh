@@ -381,6 +381,8 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
             op.push(out);
             for (int j = 1; j < n; ++j) op.push(val(sb + j));
             out = op.result();
+          } else {
+            out = lse_unary(out);
           }
         } else {
           for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));

@@ -404,3 +404,7 @@ def test_log_domain_nonfinite_inputs_match_oracle(cuda, name, eps):
     g = plan.backward(vals, B, _lib.KLAY_LOG, np.float64)
     rel_close(out.cpu().numpy(), ref, 1e-12, 1e-12)
     rel_close(g.cpu().numpy(), gref, 1e-10, 1e-12)
+    from paper_2410_11415_b200.engine import _NodeValues
+    nv = _NodeValues(plan, vals, B)
+    for l in range(len(tr)):
+        rel_close(nv[l], tr[l], 1e-12, 1e-12)
