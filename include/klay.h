@@ -104,6 +104,11 @@ KLAY_API int64_t klay_row_stride(int64_t batch, int32_t dtype);
  *   values       retain != 0: trace buffer [num_nodes, ld] (every layer kept,
  *                EvalTrace.node_values); retain == 0: scratch of
  *                2 * max_width rows (ping-pong, only the last layer survives)
+ *   retain       0: no trace; 1: full trace; 2 (KLAY_RETAIN_BACKWARD): the
+ *                trace klay_backward needs. With KLAY_LOG and epsilon 0 the
+ *                rows of unary sum nodes (a copy of their only child) are
+ *                then left unwritten: neither layer above nor klay_backward
+ *                reads them. klay_fill_trace() writes them on demand.
  *   outputs      device [B, R] row-major, element type `dtype` (may be NULL)
  *   epsilon      log semiring only, added inside the log (must be >= 0)
  *   workspace    device scratch of klay_forward_workspace() bytes (may be
@@ -113,6 +118,15 @@ KLAY_API int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
                  const void* weights, int32_t weights_dtype, void* values, int64_t ld,
                  int32_t retain, void* outputs, int64_t batch, double epsilon,
                  void* workspace, void* stream);
+
+#define KLAY_RETAIN_BACKWARD 2
+
+/* Completes a retain = 2 trace of klay_forward(semiring, epsilon): writes the
+ * rows of unary sum nodes from their children (logsumexp of one element: the
+ * child, NaN for +inf). No-op for traces that left nothing out (any
+ * semiring but KLAY_LOG, epsilon != 0). */
+KLAY_API int klay_fill_trace(const KlayPlan* plan, int32_t semiring, int32_t dtype, void* values,
+                    int64_t ld, int64_t batch, double epsilon, void* stream);
 
 /* Scratch bytes klay_forward needs for row stride `ld` (leaf partials of
  * segments longer than 129 edges, split in numpy pairwise-tree order). */
@@ -131,10 +145,15 @@ KLAY_API size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int6
  *                unary sum parents skip their value reads (their weight
  *                exp(child - parent) is then exactly 1, or 0 at -inf); any
  *                other value, e.g. -1 when unknown, reads every parent.
+ *   retain       the retain mode klay_forward wrote the trace with (1 full,
+ *                2 backward-only). A backward-only log trace with epsilon 0
+ *                carries, in the rows of unary sums, the finiteness masks
+ *                this backward uses to send their adjoints straight to
+ *                their children; pass 1 for any other (e.g. uploaded) trace.
  */
 KLAY_API int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                   int64_t ld, const void* seed, void* grads, void* workspace,
-                  int64_t batch, double epsilon, void* stream);
+                  int64_t batch, double epsilon, int32_t retain, void* stream);
 
 KLAY_API size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 

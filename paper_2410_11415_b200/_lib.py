@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libklay.so")
 KLAY_OK, KLAY_EINVAL, KLAY_EFORMAT, KLAY_ECUDA, KLAY_EUNSUPPORTED = range(5)
 KLAY_REAL, KLAY_LOG, KLAY_BOOL, KLAY_MAXPROD = range(4)
 KLAY_F32, KLAY_F64, KLAY_U1 = 0, 1, 2
+KLAY_RETAIN_BACKWARD = 2
 
 _c_i64 = ctypes.c_int64
 _c_i32 = ctypes.c_int32
@@ -36,8 +37,10 @@ SIGNATURES = {
                                     _c_i64, ctypes.c_double, _vp, _vp]),
     "klay_forward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
     "klay_backward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _vp, _vp, _vp, _c_i64,
-                                      ctypes.c_double, _vp]),
+                                      ctypes.c_double, _c_i32, _vp]),
     "klay_backward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
+    "klay_fill_trace": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _c_i64, ctypes.c_double,
+                                        _vp]),
     "klay_layerize": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_vp)]),
     "klay_layered_info": (_c_i64, [_vp, _c_i32]),

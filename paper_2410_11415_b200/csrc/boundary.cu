@@ -111,6 +111,25 @@ void launch_seed(const T* seed, const int* top_off, const int* top_pos, T* g, in
   seed_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, top_off, top_pos, g, WL, R, B, ld);
 }
 
+// Rows of unary sum nodes a backward-only trace left unwritten: the child's
+// row as a logsumexp of one element (+inf -> NaN). One thread per element.
+template <typename T>
+__global__ void fill_aliases_kernel(const int2* __restrict__ pairs, long long n, T* values,
+                                    long long ld) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * ld) return;
+  const long long k = i / ld, c = i - k * ld;
+  const int2 pr = pairs[k];
+  const T v = values[(size_t)pr.y * ld + c];
+  values[(size_t)pr.x * ld + c] = (v == T(INFINITY)) ? T(NAN) : v;
+}
+
+template <typename T>
+void launch_fill_aliases(const int2* pairs, long long n, T* values, long long ld, cudaStream_t s) {
+  const long long m = n * ld;
+  if (m > 0) fill_aliases_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(pairs, n, values, ld);
+}
+
 #define KLAY_INST(T)                                                                            \
   template void launch_load_inputs<T>(const void*, bool, T*, int, long long, long long, T,      \
                                       cudaStream_t);                                            \
@@ -118,7 +137,8 @@ void launch_seed(const T* seed, const int* top_off, const int* top_pos, T* g, in
   template void launch_assemble_outputs<T>(const T*, const int*, const signed char*, T*, int,   \
                                            long long, long long, T, T, cudaStream_t);           \
   template void launch_seed<T>(const T*, const int*, const int*, T*, int, int, long long,       \
-                               long long, cudaStream_t);
+                               long long, cudaStream_t);                                        \
+  template void launch_fill_aliases<T>(const int2*, long long, T*, long long, cudaStream_t);
 KLAY_INST(float)
 KLAY_INST(double)
 #undef KLAY_INST

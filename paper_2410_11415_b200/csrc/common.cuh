@@ -16,10 +16,12 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace klay {
 
 enum { SR_REAL = 0, SR_LOG = 1, SR_BOOL = 2, SR_MAXPROD = 3 };
-enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2 };
+enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2, BW_PASSA = 3 };
 // reduction kinds
 enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4, RK_AND = 5, RK_OR = 6 };
 
@@ -229,8 +231,10 @@ __device__ __forceinline__ void lse_merge(T& m, T& t, T m2, T t2) {
 // +inf element becomes NaN (log(0) + inf, engine.py:274-282)
 template <typename T>
 __device__ __forceinline__ Vec<T> lse_unary(Vec<T> x) {
+  if constexpr (std::is_floating_point<T>::value) {
 #pragma unroll
-  for (int c = 0; c < Vec<T>::N; ++c) x.v[c] = (x.v[c] == T(INFINITY)) ? T(NAN) : x.v[c];
+    for (int c = 0; c < Vec<T>::N; ++c) x.v[c] = (x.v[c] == T(INFINITY)) ? T(NAN) : x.v[c];
+  }
   return x;
 }
 

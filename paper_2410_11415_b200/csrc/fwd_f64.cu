@@ -3,8 +3,10 @@
 
 namespace klay {
 
-int launch_forward_layer(int sr, bool prod, const LayerArgs<double>& a, cudaStream_t s) {
+int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<double>& a, cudaStream_t s) {
   using G = FwdGather<double>;
+  // product layer over an aliased sum layer (log semiring, epsilon 0)
+  if (alias) return launch_layer<double, RK_SUM, FwdGather<double, true>>(a, s);
   switch (sr) {
     case SR_REAL:
       if (prod) return launch_layer<double, RK_PROD, G>(a, s);

@@ -22,7 +22,7 @@ using namespace klay;
 namespace {
 
 enum { SR_REAL_ = 0, SR_LOG_ = 1 };
-enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2 };
+enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2, BW_PASSA_ = 3 };
 
 // work-item shape (see layer_kernels.cuh)
 constexpr int TASK_EDGES_H = 64;   // edges per short task (<= TASK_EDGES)
@@ -72,6 +72,12 @@ void tail_trace_dump(const char* what, int n) {
 
 const bool g_no_tail = [] {
   const char* e = getenv("KLAY_NO_TAIL");
+  return e && *e && *e != '0';
+}();
+
+// KLAY_NO_ALIAS=1: every sum row is computed and read (A/B switch)
+const bool g_no_alias = [] {
+  const char* e = getenv("KLAY_NO_ALIAS");
   return e && *e && *e != '0';
 }();
 
@@ -213,6 +219,12 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   s.masks.insert(s.masks.end(), short_masks.begin(), short_masks.end());
 }
 
+// a compacted item set over a subset of a layer's nodes (unary-sum aliases)
+struct AliasSet {
+  int64_t off_base = 0, e_base = 0, map_base = 0;  // into aoff[] / aidx[] / omap[]
+  int64_t i_base = 0, i_n = 0, h_base = 0, h_n = 0, slots = 0;
+};
+
 struct LayerDesc {
   int64_t W, Wprev, E;
   bool prod;
@@ -223,6 +235,24 @@ struct LayerDesc {
   int64_t fi_base, fi_n, fh_base, fh_n, f_slots;  // forward items / heavy
   int64_t fq_base, fq_n;                           // forward items, no split (PROD)
   int64_t bi_base, bi_n, bh_base, bh_n, b_slots;  // backward items / heavy
+  // Unary-sum aliases (log semiring, epsilon 0). A sum node with one child
+  // has exactly its child's value (logsumexp of one element; +inf -> NaN),
+  // so with a backward-only trace (klay_forward retain = 2) such rows are
+  // never written:
+  //   alias_s  sum layer S: the forward computes only its non-unary nodes
+  //            (fa); the backward skips children whose only parent is unary
+  //            (ba), their adjoints come from the layer above
+  //   alias_q  product layer Q over S: forward operands of unary S nodes
+  //            read the child row two layers down (remapped sources, rows
+  //            >= W_S); the backward writes the adjoint of a unary S node
+  //            whose child has no other parent straight into that child's
+  //            row (omap bit 31), weighted by 1, or 0 for a non-finite child
+  //   mask_p   product layer P below an aliased S: its nodes whose only
+  //            parent is unary store their finiteness bits into that
+  //            parent's (unwritten) row, for the backward's alias weights
+  bool alias_s, alias_q, mask_p;
+  AliasSet fa, ba;
+  int64_t qa_e_base, qb_map_base, mrow_base;
 };
 
 struct DeviceGuard {
@@ -262,6 +292,11 @@ struct KlayPlan {
   signed char* d_const = nullptr;
   int* d_top_off = nullptr;
   int* d_top_pos = nullptr;
+  int* d_aoff = nullptr;   // unary-sum aliases: compacted offsets,
+  int* d_aidx = nullptr;   // compacted / remapped edge indices,
+  int* d_omap = nullptr;   // item node -> node id maps
+  int2* d_alias = nullptr;  // {trace row of a unary sum, trace row of its child}
+  int64_t n_alias = 0;
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
   int32_t tail_from = 0;  // first layer of the persistent tail (L = no tail)
 };
@@ -283,6 +318,10 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_const);
   cudaFree(p->d_top_off);
   cudaFree(p->d_top_pos);
+  cudaFree(p->d_aoff);
+  cudaFree(p->d_aidx);
+  cudaFree(p->d_omap);
+  cudaFree(p->d_alias);
   delete p;
 }
 
@@ -317,6 +356,24 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   std::vector<int> off, src, toff, tpar;
   std::vector<int4> items, heavy;
   std::vector<unsigned> masks;  // parallel to items
+  std::vector<int> aoff, aidx, omap;
+  std::vector<int2> alias_rows;
+  // the previous layer when it is an aliased sum layer: child of each unary
+  // node (-1 otherwise) and whether that child has no other parent
+  std::vector<int> s_child;
+  std::vector<char> s_full;
+  bool s_open = false;
+  int64_t s_W = 0;
+  auto add_set = [&](ItemSet& set, AliasSet& as) {
+    as.i_base = (int64_t)items.size();
+    as.i_n = (int64_t)set.items.size();
+    items.insert(items.end(), set.items.begin(), set.items.end());
+    masks.insert(masks.end(), set.masks.begin(), set.masks.end());
+    as.h_base = (int64_t)heavy.size();
+    as.h_n = (int64_t)set.heavy.size();
+    heavy.insert(heavy.end(), set.heavy.begin(), set.heavy.end());
+    as.slots = set.slots;
+  };
   // the tail: longest suffix of layers with <= TAIL_EDGES edges
   int32_t tail_from = num_layers;
   while (tail_from > 0 && num_layers - tail_from < TAIL_MAX_LAYERS &&
@@ -418,6 +475,79 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.b_slots = bs.slots;
     p->max_fslots = std::max<int64_t>(p->max_fslots, fs.slots);
     p->max_bslots = std::max<int64_t>(p->max_bslots, bs.slots);
+    // ---- unary-sum aliases (see LayerDesc) ----
+    if (d.prod && s_open) {
+      // Q over the aliased sum layer below: remapped forward sources and the
+      // backward child map
+      d.alias_q = true;
+      d.qa_e_base = (int64_t)aidx.size();
+      for (int64_t e = 0; e < E; ++e)
+        aidx.push_back(s_child[S[e]] >= 0 ? (int)(s_W + s_child[S[e]]) : (int)S[e]);
+      d.qb_map_base = (int64_t)omap.size();
+      for (int64_t j = 0; j < s_W; ++j)
+        omap.push_back(s_full[j] ? (s_child[j] | INT32_MIN) : (int)j);
+    }
+    s_open = false;
+    if (!d.prod && l + 1 < num_layers && l + 1 < tail_from && W + prev_w < (1LL << 31)) {
+      d.alias_s = true;
+      s_child.assign(W, -1);
+      s_full.assign(W, 0);
+      for (int64_t i = 0; i < W; ++i) {
+        if (cnt[i] != 1) continue;
+        const int c = (int)S[off[d.off_base + i]];
+        s_child[i] = c;
+        s_full[i] = gcnt[c] == 1;
+        alias_rows.push_back(make_int2((int)(d.row + i), (int)(d.prev_row + c)));
+      }
+      // forward: the non-unary parents only
+      ItemSet fa, ba;
+      d.fa.off_base = (int64_t)aoff.size();
+      d.fa.e_base = (int64_t)aidx.size();
+      d.fa.map_base = (int64_t)omap.size();
+      aoff.push_back(0);
+      int64_t nc = 0, ec = 0;
+      for (int64_t i = 0; i < W; ++i) {
+        if (cnt[i] == 1) continue;
+        for (int e = off[d.off_base + i]; e < off[d.off_base + i + 1]; ++e) aidx.push_back((int)S[e]);
+        ec += cnt[i];
+        aoff.push_back((int)ec);
+        omap.push_back((int)i);
+        ++nc;
+      }
+      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0);
+      add_set(fa, d.fa);
+      // backward: children that are not the only child of a unary parent
+      d.ba.off_base = (int64_t)aoff.size();
+      d.ba.e_base = (int64_t)aidx.size();
+      d.ba.map_base = (int64_t)omap.size();
+      aoff.push_back(0);
+      nc = 0;
+      ec = 0;
+      for (int64_t j = 0; j < prev_w; ++j) {
+        const int t0 = toff[d.toff_base + j], t1 = toff[d.toff_base + j + 1];
+        if (t1 - t0 == 1 && cnt[tpar[tb + t0] & 0x7fffffff] == 1) continue;  // alias target
+        for (int t = t0; t < t1; ++t) aidx.push_back(tpar[tb + t]);
+        ec += t1 - t0;
+        aoff.push_back((int)ec);
+        omap.push_back((int)j);
+        ++nc;
+      }
+      build_items(aoff, (size_t)d.ba.off_base, (int)nc, SHORT_BWD, ba, true, 0);
+      add_set(ba, d.ba);
+      // the product layer below keeps the finiteness masks of alias targets
+      LayerDesc& dp = p->layers.back();
+      dp.mask_p = true;
+      dp.mrow_base = (int64_t)omap.size();
+      std::vector<int> mrow(prev_w, -1);
+      for (int64_t i = 0; i < W; ++i)
+        if (s_full[i]) mrow[s_child[i]] = (int)i;
+      omap.insert(omap.end(), mrow.begin(), mrow.end());
+      p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
+      p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
+      p->max_heavy = std::max<int64_t>(p->max_heavy, std::max(fa.heavy.size(), ba.heavy.size()));
+      s_open = true;
+      s_W = W;
+    }
     p->layers.push_back(d);
     p->layer_row.push_back(row);
     p->max_width = std::max(p->max_width, W);
@@ -427,6 +557,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   }
   p->total_rows = row;
   p->WL = prev_w;
+  p->n_alias = (int64_t)alias_rows.size();
 
   // roots (engine.py:203-212, 330-334)
   std::vector<int> rn(num_roots);
@@ -452,7 +583,9 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       (rc = upload(&p->d_items, items)) || (rc = upload(&p->d_masks, masks)) ||
       (rc = upload(&p->d_heavy, heavy)) ||
       (rc = upload(&p->d_root_node, rn)) || (rc = upload(&p->d_const, cv)) ||
-      (rc = upload(&p->d_top_off, top_off)) || (rc = upload(&p->d_top_pos, top_pos))) {
+      (rc = upload(&p->d_top_off, top_off)) || (rc = upload(&p->d_top_pos, top_pos)) ||
+      (rc = upload(&p->d_aoff, aoff)) || (rc = upload(&p->d_aidx, aidx)) ||
+      (rc = upload(&p->d_omap, omap)) || (rc = upload(&p->d_alias, alias_rows))) {
     plan_free(p);
     return rc;
   }
@@ -497,7 +630,7 @@ extern "C" size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, in
 
 extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
   if (!plan) return 0;
-  return ((size_t)2 * plan->max_width + plan->max_bslots) * ld * esize(dtype) +
+  return ((size_t)3 * plan->max_width + plan->max_bslots) * ld * esize(dtype) +
          counter_bytes(plan, dtype, ld);
 }
 
@@ -523,7 +656,8 @@ LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, 
 
 template <typename T>
 int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* values, int64_t ld,
-                 bool retain, void* outputs, int64_t B, double eps, T* work, cudaStream_t s) {
+                 int retain_mode, void* outputs, int64_t B, double eps, T* work, cudaStream_t s) {
+  const bool retain = retain_mode != 0;
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* pingpong[2] = {values, values + (size_t)p->max_width * ld};
   constexpr bool U1 = std::is_same<T, unsigned>::value;
@@ -551,10 +685,34 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     tail->debug_skip = g_tail_debug ? 1 : 0;
     tail->trace_ts = g_tail_trace ? tail_trace_buf() : nullptr;
   }
+  // unary-sum aliases need the rows two layers down: backward-only traces
+  constexpr bool U1_ = std::is_same<T, unsigned>::value;
+  const bool alias = !U1_ && sr == SR_LOG_ && eps == 0.0 && retain_mode == 2 && !g_no_alias;
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
     LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
+    const bool alias_q = alias && d.alias_q;
+    if (alias && d.alias_s) {
+      // non-unary parents only (compacted CSR, node ids via omap)
+      a.items = p->d_items + d.fa.i_base;
+      a.masks = p->d_masks + d.fa.i_base;
+      a.n_items = (int)d.fa.i_n;
+      a.heavy = p->d_heavy + d.fa.h_base;
+      a.n_heavy = (int)d.fa.h_n;
+      a.off = p->d_aoff + d.fa.off_base;
+      a.idx = p->d_aidx + d.fa.e_base;
+      a.omap = p->d_omap + d.fa.map_base;
+    }
+    if (alias_q) {
+      a.idx = p->d_aidx + d.qa_e_base;
+      a.prev2 = values + (size_t)p->layers[l - 2].row * ld;
+      a.nsplit = (int)p->layers[l - 1].W;
+    }
+    if (alias && d.mask_p) {
+      a.mrow = p->d_omap + d.mrow_base;
+      a.mbase = values + (size_t)p->layers[l + 1].row * ld;
+    }
     if (d.prod && (sr == SR_REAL_ || sr == KLAY_MAXPROD)) {
       // sequential product: heavy segments stay whole (no leaves, no combine)
       a.items = p->d_items + d.fq_base;
@@ -573,7 +731,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       a.hcount = hcount;
       LaunchScope ls(s, 0, l + 1);
       if constexpr (U1) g_launches += launch_forward_layer_u1(d.prod, a, s);
-      else g_launches += launch_forward_layer(sr, d.prod, a, s);
+      else g_launches += launch_forward_layer(sr, d.prod, alias_q, a, s);
     }
     prev = cur;
   }
@@ -622,21 +780,25 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
 
 template <typename T>
 int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, const T* seed,
-                  T* grads, T* work, int64_t B, double epsilon, cudaStream_t s) {
+                  T* grads, T* work, int64_t B, double epsilon, int retain_mode, cudaStream_t s) {
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
-  T* g[2] = {work, work + (size_t)p->max_width * ld};
-  T* scratch = work + (size_t)2 * p->max_width * ld;
+  // adjoints of node layer n (0 = inputs .. L) live in gb[n % 3]: a layer
+  // kernel reads layer l+1's and writes layer l's; alias outputs of a
+  // product layer go one further down, to layer l-1's
+  T* gb[3] = {work, work + (size_t)p->max_width * ld, work + (size_t)2 * p->max_width * ld};
+  T* scratch = work + (size_t)3 * p->max_width * ld;
   int* hcount = reinterpret_cast<int*>(scratch + (size_t)p->max_bslots * ld);
   if (p->max_heavy > 0) {
     const size_t nb = counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld);
     KLAY_CUDA(cudaMemsetAsync(hcount, 0, nb, s));
   }
-  int cur = 0;
   {
     LaunchScope ls(s, 3, p->L + 1);
-    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, g[cur], (int)p->WL, p->R, B, ld, s);
+    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, gb[p->L % 3], (int)p->WL, p->R, B, ld, s);
     ++g_launches;
   }
+  // alias outputs need the finiteness masks of a backward-only trace
+  const bool alias = domain == SR_LOG_ && epsilon == 0.0 && retain_mode == 2 && !g_no_alias;
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
   TailArgs<T>* tail = nullptr;
   if (tail_from < p->L) {
@@ -648,8 +810,8 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
     LayerArgs<T> a = layer_args<T>(p, d, false, V, ld);
-    a.out = g[cur ^ 1];
-    a.gcur = g[cur];
+    a.out = gb[l % 3];
+    a.gcur = gb[(l + 1) % 3];
     a.ncur = trace + (size_t)d.row * ld;
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
@@ -685,14 +847,29 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       int mode = BW_PASS_;
       if (domain == SR_REAL_ && d.prod) mode = BW_REALPROD_;
       else if (domain == SR_LOG_ && !d.prod) mode = BW_LOGSUM_;
+      if (alias && d.alias_s) {
+        // children that are not the only child of a unary parent
+        a.items = p->d_items + d.ba.i_base;
+        a.masks = p->d_masks + d.ba.i_base;
+        a.n_items = (int)d.ba.i_n;
+        a.heavy = p->d_heavy + d.ba.h_base;
+        a.n_heavy = (int)d.ba.h_n;
+        a.off = p->d_aoff + d.ba.off_base;
+        a.idx = p->d_aidx + d.ba.e_base;
+        a.omap = p->d_omap + d.ba.map_base;
+      }
+      if (alias && d.alias_q) {
+        mode = BW_PASSA_;
+        a.omap = p->d_omap + d.qb_map_base;
+        a.out2 = gb[(l - 1) % 3];
+      }
       LaunchScope ls(s, 1, l + 1);
       g_launches += launch_backward_layer(mode, a, s);
     }
-    cur ^= 1;
   }
   if (p->K > 0) {
     LaunchScope ls(s, 3, 0);
-    launch_store_rows<T>(g[cur], grads, (int)p->K, B, ld, s);
+    launch_store_rows<T>(gb[0], grads, (int)p->K, B, ld, s);
     ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());
@@ -716,6 +893,7 @@ extern "C" int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtyp
                             void* workspace, void* stream) {
   if (int rc = check_common(plan, dtype, batch, ld)) return rc;
   if (semiring < KLAY_REAL || semiring > KLAY_MAXPROD) return fail(KLAY_EINVAL, "unknown semiring");
+  if (retain < 0 || retain > 2) return fail(KLAY_EINVAL, "retain must be 0, 1 or 2");
   if (weights_dtype != KLAY_F32 && weights_dtype != KLAY_F64) return fail(KLAY_EINVAL, "unknown weights dtype");
   if (semiring == KLAY_LOG && !(epsilon >= 0)) return fail(KLAY_EINVAL, "epsilon must be >= 0");
   if (!values || (plan->K > 0 && !weights)) return fail(KLAY_EINVAL, "NULL buffer");
@@ -730,15 +908,15 @@ extern "C" int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtyp
                                   retain != 0, outputs, batch, 0.0, (unsigned*)workspace, s);
   }
   if (dtype == KLAY_F32)
-    return forward_impl<float>(plan, semiring, weights, weights_dtype, (float*)values, ld, retain != 0,
+    return forward_impl<float>(plan, semiring, weights, weights_dtype, (float*)values, ld, retain,
                                outputs, batch, epsilon, (float*)workspace, s);
-  return forward_impl<double>(plan, semiring, weights, weights_dtype, (double*)values, ld, retain != 0,
+  return forward_impl<double>(plan, semiring, weights, weights_dtype, (double*)values, ld, retain,
                               outputs, batch, epsilon, (double*)workspace, s);
 }
 
 extern "C" int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                              int64_t ld, const void* seed, void* grads, void* workspace, int64_t batch,
-                             double epsilon, void* stream) {
+                             double epsilon, int32_t retain, void* stream) {
   if (int rc = check_common(plan, dtype, batch, ld)) return rc;
   if (dtype == KLAY_U1) return fail(KLAY_EUNSUPPORTED, "no backward for bit-packed Boolean rows");
   if (domain != KLAY_REAL && domain != KLAY_LOG)
@@ -750,9 +928,25 @@ extern "C" int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (dtype == KLAY_F32)
     return backward_impl<float>(plan, domain, (const float*)trace, ld, (const float*)seed, (float*)grads,
-                                (float*)workspace, batch, epsilon, s);
+                                (float*)workspace, batch, epsilon, retain, s);
   return backward_impl<double>(plan, domain, (const double*)trace, ld, (const double*)seed,
-                               (double*)grads, (double*)workspace, batch, epsilon, s);
+                               (double*)grads, (double*)workspace, batch, epsilon, retain, s);
+}
+
+extern "C" int klay_fill_trace(const KlayPlan* plan, int32_t semiring, int32_t dtype, void* values,
+                               int64_t ld, int64_t batch, double epsilon, void* stream) {
+  if (int rc = check_common(plan, dtype, batch, ld)) return rc;
+  if (!values) return fail(KLAY_EINVAL, "NULL buffer");
+  // only log-semiring, epsilon-0 traces leave rows out (forward_impl)
+  if (semiring != KLAY_LOG || epsilon != 0.0 || dtype == KLAY_U1 || g_no_alias || plan->n_alias == 0)
+    return KLAY_OK;
+  DeviceGuard guard(plan->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == KLAY_F32) launch_fill_aliases<float>(plan->d_alias, plan->n_alias, (float*)values, ld, s);
+  else launch_fill_aliases<double>(plan->d_alias, plan->n_alias, (double*)values, ld, s);
+  ++g_launches;
+  KLAY_CUDA(cudaGetLastError());
+  return KLAY_OK;
 }
 
 extern "C" int64_t klay_launch_count(void) { return g_launches.load(); }

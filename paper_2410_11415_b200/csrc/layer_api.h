@@ -33,6 +33,18 @@ struct LayerArgs {
   int unary_ok;       // backward: edges flagged as unary parents need no parent value
   int* hcount;        // per (heavy segment, chunk) leaf counters: the last leaf combines
                       // (null: a separate combine pass / the tail's own barrier)
+  // unary-sum aliasing (klay.cu, "aliases"); all null/0 when off
+  const int* omap;    // item node j -> output/own-value row; bit 31: alias output
+                      // (backward pass-through: row of out2, masked by xalt)
+  T* out2;            // alias outputs (adjoints of the layer two below)
+  const T* prev2;     // forward: operand rows >= nsplit live here (row - nsplit)
+  int nsplit;
+  // forward of a product layer below an aliased sum layer: node j whose only
+  // parent is a unary sum (row mrow[j] >= 0 of mbase, a row the forward
+  // leaves unwritten) also stores there the finiteness bits of its value,
+  // the only part of it the backward's alias outputs (PASSA) need
+  const int* mrow;
+  T* mbase;
 };
 
 // The persistent tail kernel (thin upper layers in one launch) takes its
@@ -51,8 +63,8 @@ struct TailArgs {
 };
 
 // forward layer: semiring x layer op -> reduction kind (RK_*)
-int launch_forward_layer(int sr, bool prod, const LayerArgs<float>& a, cudaStream_t s);
-int launch_forward_layer(int sr, bool prod, const LayerArgs<double>& a, cudaStream_t s);
+int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<float>& a, cudaStream_t s);
+int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<double>& a, cudaStream_t s);
 // backward layer (BW_* mode): always a pairwise sum over each child's out-edges
 int launch_backward_layer(int mode, const LayerArgs<float>& a, cudaStream_t s);
 int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s);
@@ -89,5 +101,7 @@ void launch_assemble_outputs(const T* last, const int* root_node, const signed c
 template <typename T>
 void launch_seed(const T* seed, const int* top_off, const int* top_pos, T* g, int WL, int R,
                  long long B, long long ld, cudaStream_t s);
+template <typename T>
+void launch_fill_aliases(const int2* pairs, long long n, T* values, long long ld, cudaStream_t s);
 
 }  // namespace klay

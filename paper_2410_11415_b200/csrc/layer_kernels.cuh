@@ -21,6 +21,9 @@ constexpr int WARPS_PER_BLOCK = 4;
 #ifndef KLAY_PASS_MINB
 #define KLAY_PASS_MINB 5  // resident blocks of the pass-through backward kernel
 #endif
+#ifndef KLAY_FWD_MINB
+#define KLAY_FWD_MINB 6
+#endif
 #ifndef KLAY_LOGSUM_MINB
 #define KLAY_LOGSUM_MINB 1
 #endif
@@ -32,35 +35,90 @@ constexpr int WARPS_PER_BLOCK = 4;
 // value():  the edge's contribution, from the staged operands
 // NX:       a per-node own value is staged too (backward: the child's x)
 
+// ---- finiteness bit masks (unary-sum aliases) --------------------------------
+// Word e of a column chunk's mask holds bit l = isfinite(element e of lane l's
+// vector); NV 16-byte pieces per chunk, written by lane 0 at the chunk's
+// first column. All 32 lanes must call store_mask (ballots).
 template <typename T>
-struct FwdGather {
-  static constexpr int NOP = 1, NX = 0, SE = 8;
-  static constexpr int MINB = 6;  // resident blocks per SM (shared memory allows 6)
-  const T* base;
-  long long ld;
-  int nl;
-  __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col, int nl_)
-      : base(a.prev + col), ld(a.ld), nl(nl_) {}
-  __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
-    cp_async_vec(slot, lane, base + (size_t)row * ld, nl);
+__device__ __forceinline__ void store_mask(T* chunk0, const Vec<T>& v, int lane) {
+  constexpr int N = Vec<T>::N;
+  unsigned w[(N + 3) / 4 * 4];
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    bool fin = true;
+    if constexpr (std::is_floating_point<T>::value) fin = isfinite(v.v[e]);
+    w[e] = __ballot_sync(0xffffffffu, fin);
   }
-  __device__ __forceinline__ void issue_x(uint4*, int, int) const {}
-  __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int, const Vec<T>&) const {
-    return lds_vec<T>(slot, lane);
+#pragma unroll
+  for (int e = N; e < (N + 3) / 4 * 4; ++e) w[e] = 0u;
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < (N + 3) / 4; ++q)
+      reinterpret_cast<uint4*>(chunk0)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+}
+// a stand-in own value with the mask's finiteness: 0 (finite) or -inf
+template <typename T>
+__device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
+  Vec<T> x;
+#pragma unroll
+  for (int e = 0; e < Vec<T>::N; ++e) {
+    if constexpr (std::is_floating_point<T>::value) x.v[e] = ((w[e] >> lane) & 1u) ? T(0) : T(-INFINITY);
+    else x.v[e] = T(0);
+  }
+  return x;
+}
+
+// ALIAS (log semiring, epsilon 0): operand rows >= nsplit are unary sums of
+// the layer below that the forward never wrote; they read their child's row
+// in prev2 instead, as logsumexp of one element (x, or NaN for +inf)
+template <typename T, bool ALIAS = false>
+struct FwdGather {
+  static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
+  static constexpr bool ROWV = ALIAS, ALIAS_OUT = false;
+  static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 6)
+  const T* base;
+  const T* base2;
+  long long ld;
+  int nl, nsplit;
+  __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col, int nl_)
+      : base(a.prev + col), base2(ALIAS ? a.prev2 + col : nullptr), ld(a.ld), nl(nl_),
+        nsplit(a.nsplit) {}
+  __device__ __forceinline__ const T* row_ptr(int row) const {
+    if (ALIAS && row >= nsplit) return base2 + (size_t)(row - nsplit) * ld;
+    return base + (size_t)row * ld;
+  }
+  __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
+    cp_async_vec(slot, lane, row_ptr(row), nl);
+  }
+  __device__ __forceinline__ void issue_x(uint4*, int, int, int) const {}
+  __device__ __forceinline__ Vec<T> x_from_stage(const uint4*, int) const { return Vec<T>{}; }
+  __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>&) const {
+    const Vec<T> v = lds_vec<T>(slot, lane);
+    return (ALIAS && row >= nsplit) ? lse_unary(v) : v;
   }
   __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>&) const {
-    return ldv(base + (size_t)row * ld, nl);
+    const Vec<T> v = ldv(row_ptr(row), nl);
+    return (ALIAS && row >= nsplit) ? lse_unary(v) : v;
   }
-  __device__ __forceinline__ Vec<T> load_x(int) const { return Vec<T>{}; }
+  __device__ __forceinline__ Vec<T> load_x(int, int) const { return Vec<T>{}; }
 };
 
+// PASSA: pass-through whose children may be alias outputs (omap bit 31): the
+// adjoint of a unary sum goes straight to its only child, two layers down,
+// with the unary softmax weight: 1, or 0 for a non-finite child value, read
+// from the finiteness mask the forward left in the unary sum's own row
 template <typename T, int MODE>
 struct BwdGather {
-  static constexpr int NOP = (MODE == BW_PASS) ? 1 : 2;
+  static constexpr bool PASSLIKE = (MODE == BW_PASS || MODE == BW_PASSA);
+  static constexpr int NOP = PASSLIKE ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
+  static constexpr bool ROWV = (NOP == 2), ALIAS_OUT = (MODE == BW_PASSA);
   static constexpr int SE = 8;
-  static constexpr int MINB = (NOP == 1) ? KLAY_PASS_MINB            // (6 blocks: spills)
-                              : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB : 1);
+  static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
+  static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
+                              : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
+                                                   : (MODE == BW_PASSA ? 3 : 1));  // (smem: 3)
   const T* gbase;
   const T* nbase;
   const T* xbase;
@@ -70,8 +128,10 @@ struct BwdGather {
   int nl;
   bool unary_ok;
   __device__ __forceinline__ BwdGather(const LayerArgs<T>& a, size_t col, int nl_)
-      : gbase(a.gcur + col), nbase(a.ncur + col), xbase(a.nprev + col), foff(a.foff),
-        fsrc(a.fsrc), ld(a.ld), nl(nl_), unary_ok(a.unary_ok != 0) {}
+      : gbase(a.gcur + col), nbase(a.ncur + col),
+        // PASSA: the masks sit at the column chunk's start of the child rows
+        xbase(a.nprev + (MODE == BW_PASSA ? col - (col % (32 * NV * PIECE<T>)) : col)),
+        foff(a.foff), fsrc(a.fsrc), ld(a.ld), nl(nl_), unary_ok(a.unary_ok != 0) {}
   // Edge rows of the transposed CSR carry bit 31 when the parent is a unary
   // sum (klay.cu plan build); with epsilon 0 such a parent's value equals the
   // child's, so LOGSUM skips loading it (unary_ok) and every mode masks the bit.
@@ -84,10 +144,33 @@ struct BwdGather {
     if constexpr (NOP == 2)
       if (!unary_edge(row)) cp_async_vec(slot + NV * 32, lane, nbase + r * ld, nl);
   }
-  __device__ __forceinline__ void issue_x(uint4* slot, int node, int lane) const {
-    cp_async_vec(slot, lane, xbase + (size_t)node * ld, nl);
+  // own value of node id `node` (item node `j`). PASSA: alias outputs only,
+  // as the finiteness mask in child row j (see store_mask)
+  __device__ __forceinline__ void issue_x(uint4* slot, int node, int j, int lane) const {
+    if (MODE == BW_PASSA) {
+      if (node < 0 && lane < NV)
+        cp_async16(slot + lane, xbase + (size_t)j * ld + lane * (16 / sizeof(T)));
+    } else {
+      cp_async_vec(slot, lane, xbase + (size_t)node * ld, nl);
+    }
   }
-  __device__ __forceinline__ Vec<T> load_x(int node) const { return ldv(xbase + (size_t)node * ld, nl); }
+  __device__ __forceinline__ Vec<T> x_from_stage(const uint4* slot, int lane) const {
+    if (MODE == BW_PASSA) return mask_to_x<T>(reinterpret_cast<const unsigned*>(slot), lane);
+    return lds_vec<T>(slot, lane);
+  }
+  __device__ __forceinline__ Vec<T> load_x(int node, int j) const {
+    if (MODE == BW_PASSA) {
+      if (node >= 0) return Vec<T>{};
+      unsigned w[NV * 4];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(xbase + (size_t)j * ld) + q);
+        w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
+      }
+      return mask_to_x<T>(w, (int)(threadIdx.x & 31));
+    }
+    return ldv(xbase + (size_t)node * ld, nl);
+  }
   __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>& x) const {
     if constexpr (NOP == 2) {
       if (unary_edge(row)) return unary(lds_vec<T>(slot, lane), x);
@@ -190,17 +273,29 @@ struct BwdGather {
 constexpr int TASK_EDGES = 128;  // max staged edge indices per item (longer items read idx directly)
 constexpr int TASK_NODES = 31;   // max nodes of a short task (one lane per segment offset)
 
+// ---- per-item index data (warp-private shared memory) ----------------------
+// The structure of an item (descriptor, batch mask, edge indices, segment
+// offsets) does not depend on values: the tail kernel loads it for the next
+// layer while the cluster barrier of the current layer is still open.
+struct ItemIndex {
+  int4 it;            // item descriptor (see items_kernel)
+  unsigned mask;      // short task: bit j set when node j starts a stage batch
+  int pad[3];
+  int widx[TASK_EDGES];
+  int woff[32];       // short task: segment offsets relative to it.z
+  int wmap[32];       // with LayerArgs::omap: node ids of the item's nodes
+};
+
 template <typename T, typename G>
 struct ItemsSmem {
   static constexpr int SE = G::SE;                 // edges per stage batch (= max short segment)
   // stage units: 16-byte pieces; a staged vector is NV x 32 lanes of pieces
   static constexpr int EV = G::NOP * NV * 32;      // pieces per staged edge
-  static constexpr int XV = G::NX * NV * 32;       // pieces per staged own value
+  static constexpr int XV = G::NX * G::XPIECES;    // pieces per staged own value
   static constexpr int STAGE_V = SE * (EV + XV);   // pieces per stage
   static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * 16;
-  // + one ItemIndex (sizeof = 32 + 4 * (TASK_EDGES + 32) bytes)
-  static constexpr size_t warp_bytes =
-      (stage_bytes + 32 + (size_t)4 * (TASK_EDGES + 32) + 127) / 128 * 128;
+  // + one ItemIndex
+  static constexpr size_t warp_bytes = (stage_bytes + sizeof(ItemIndex) + 127) / 128 * 128;
   static constexpr size_t bytes = warp_bytes * WARPS_PER_BLOCK;
 };
 
@@ -226,24 +321,13 @@ __device__ __forceinline__ Vec<T> combine8(const Vec<T> (&r)[8]) {
   return res;
 }
 
-// ---- per-item index data (warp-private shared memory) ----------------------
-// The structure of an item (descriptor, batch mask, edge indices, segment
-// offsets) does not depend on values: the tail kernel loads it for the next
-// layer while the cluster barrier of the current layer is still open.
-struct ItemIndex {
-  int4 it;            // item descriptor (see items_kernel)
-  unsigned mask;      // short task: bit j set when node j starts a stage batch
-  int pad[3];
-  int widx[TASK_EDGES];
-  int woff[32];       // short task: segment offsets relative to it.z
-};
-
 // registers of one lane while an ItemIndex is in flight
 struct ItemRegs {
   int4 it;
   unsigned mask;
   int idx[TASK_EDGES / 32];
   int off;
+  int map;
 };
 
 // index loads of one item whose descriptor (it, mask) is already known
@@ -261,6 +345,8 @@ __device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int4 i
   }
   const int nn = r.it.y - r.it.x;
   r.off = (r.it.y > 0 && lane <= nn) ? __ldg(a.off + r.it.x + lane) - r.it.z : 0;
+  const int* mp = a.omap ? a.omap : a.mrow;  // (never both)
+  r.map = (mp && lane < (r.it.y > 0 ? nn : 1)) ? __ldg(mp + r.it.x + lane) : 0;
   return r;
 }
 
@@ -277,6 +363,7 @@ __device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r
 #pragma unroll
   for (int q = 0; q < TASK_EDGES / 32; ++q) ib->widx[q * 32 + lane] = r.idx[q];
   ib->woff[lane] = r.off;
+  ib->wmap[lane] = r.map;
 }
 
 // Run one item (index data in `ib`, synchronized) for one 512-byte column
@@ -308,6 +395,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   constexpr int SE = S::SE, EV = S::EV, XV = S::XV, STAGE_V = S::STAGE_V;
   const int* widx = ib->widx;
   const int* woff = ib->woff;
+  const int* wmap = ib->wmap;
 
   // Lanes (pieces) past the row work on valid columns and never store: the
   // whole warp runs the same instruction stream without divergence.
@@ -326,6 +414,10 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     // batches (<= SE edges, host-computed bit mask) are staged two at a time
     // and reduced node by node
     const int nb = it.x, nn = it.y - it.x;
+    // node id of item node nd: output row / own-value row (omap: compacted
+    // item sets and alias outputs, see LayerArgs)
+    auto nid = [&](int nd) { return a.omap ? wmap[nd] : nb + nd; };
+    const size_t col0 = (size_t)chunk * 32 * NV * PIECE<T>;  // the chunk's first column
     unsigned m_issue = ib->mask, m_scan = ib->mask;
     auto next_batch = [&](unsigned& m, int& n0, int& n1) {
       n0 = __ffs(m) - 1;
@@ -339,11 +431,10 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       const int eb = woff[n0], cnt = woff[n1] - eb;
       for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, widx[eb + i], lane);
       if constexpr (G::NX)
-        for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nb + nd, lane);
+        for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nid(nd), nb + nd, lane);
       cp_async_commit();
     };
     const int nbat = __popc(ib->mask);
-    T* outp = a.out + (size_t)nb * ld + col;
     issue(0);
     for (int b = 0; b < nbat; ++b) {
       if (b + 1 < nbat) {
@@ -359,9 +450,9 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       for (int nd = n0; nd < n1; ++nd) {
         const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
         Vec<T> x{};
-        if constexpr (G::NX) x = lds_vec<T>(st + SE * EV + (nd - n0) * XV, lane);
+        if constexpr (G::NX) x = g.x_from_stage(st + SE * EV + (nd - n0) * XV, lane);
         auto val = [&](int e) {
-          return g.value(st + e * EV, lane, (G::NOP == 2) ? widx[eb + e] : 0, x);
+          return g.value(st + e * EV, lane, G::ROWV ? widx[eb + e] : 0, x);
         };
         Vec<T> out = val(sb);
         if constexpr (RK == RK_SUM) {
@@ -387,7 +478,18 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
         } else {
           for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
         }
-        stv(outp + (size_t)nd * ld, out, na);
+        const int id = nid(nd);
+        if constexpr (G::ALIAS_OUT) {
+          if (id < 0) {
+            stv(a.out2 + (size_t)(id & 0x7fffffff) * ld + col, G::unary(out, x), na);
+            continue;
+          }
+        }
+        stv(a.out + (size_t)id * ld + col, out, na);
+        if (a.mrow) {
+          const int mr = wmap[nd];
+          if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + col0, out, lane);
+        }
       }
     }
     return;
@@ -395,11 +497,11 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
 
   // ===================== long segment / leaf =====================
   const bool leaf = it.y < 0;
-  const int node = it.x;
+  const int node = a.omap ? wmap[0] : it.x;  // node id (see the short path; wmap = mrow otherwise)
   const int t0 = leaf ? 0 : 1;      // first tail edge (relative)
   const int m = ne - t0;            // tail length
   Vec<T> x{};
-  if constexpr (G::NX) x = g.load_x(node);
+  if constexpr (G::NX) x = g.load_x(node, it.x);
   auto row_of = [&](int e) { return staged_idx ? widx[e] : __ldg(a.idx + it.z + e); };
   // round t stages tail elements [8t, 8t+8)
   auto issue = [&](int t) {
@@ -435,7 +537,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
     auto val = [&](int i) {
-      return g.value(st + i * EV, lane, (G::NOP == 2) ? row_of(base + i) : 0, x);
+      return g.value(st + i * EV, lane, G::ROWV ? row_of(base + i) : 0, x);
     };
     if constexpr (RK == RK_SUM) {
       if (8 * t < mainend) {
@@ -490,11 +592,21 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       }
     }
   } else {
-    if (na == 0) return;
     Vec<T> out;
     if constexpr (RK == RK_SUM) out = (m == 0) ? x0 : vadd(x0, res);
     else if constexpr (RK == RK_LSE) out = lse.result();
     else out = acc;
+    if (a.mrow) {  // (all lanes: ballots)
+      const int mr = wmap[0];
+      if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + (size_t)chunk * 32 * NV * PIECE<T>, out, lane);
+    }
+    if (na == 0) return;
+    if constexpr (G::ALIAS_OUT) {
+      if (node < 0) {
+        stv(a.out2 + (size_t)(node & 0x7fffffff) * ld + col, G::unary(out, x), na);
+        return;
+      }
+    }
     stv(a.out + (size_t)node * ld + col, out, na);
   }
 }
@@ -537,8 +649,8 @@ inline bool pdl_enabled() {
 template <typename T, int RK, typename G>
 __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int chunk, int lane,
                                               uint4* sm, int sm_pieces) {
+  // (every lane runs to the end: stores are masked by na, mask ballots need all)
   const LaneCols lc = lane_cols<T>(a.V, chunk, lane);
-  if (lc.na == 0) return;
   const int nl = lc.nl;
   const size_t col = lc.col;
   const long long ld = a.ld;
@@ -546,8 +658,9 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
   const int node = hv.x, slot0 = hv.y, nleaf = hv.z;
   const int s = __ldg(a.off + node);
   const int n = __ldg(a.off + node + 1) - s;
+  const int id = a.omap ? __ldg(a.omap + node) : node;  // output / own-value row
   const G g(a, col, nl);
-  const Vec<T> x = g.load_x(node);
+  const Vec<T> x = g.load_x(id, node);
   const Vec<T> x0 = g.direct(__ldg(a.idx + s), x);
   Vec<T> res;
   if constexpr (RK == RK_SUM) {
@@ -581,7 +694,17 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
     for (int l = 0; l < nleaf; ++l) op.push(ldv(a.scratch + (size_t)(slot0 + l) * ld + col, nl));
     res = op.result();
   }
-  stv(a.out + (size_t)node * ld + col, res, lc.na);
+  if (a.mrow) {
+    const int mr = __ldg(a.mrow + node);
+    if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + (size_t)chunk * 32 * NV * PIECE<T>, res, lane);
+  }
+  if constexpr (G::ALIAS_OUT) {
+    if (id < 0) {
+      stv(a.out2 + (size_t)(id & 0x7fffffff) * ld + col, G::unary(res, x), lc.na);
+      return;
+    }
+  }
+  stv(a.out + (size_t)id * ld + col, res, lc.na);
 }
 
 constexpr int COMBINE_LEAVES = 64;  // leaf partials staged per combine warp

@@ -266,6 +266,9 @@ class DevicePlan:
     def forward(self, weights, semiring: int, dtype, retain=True, epsilon=0.0,
                 values=None, outputs=None, workspace=None):
         """weights: cuda tensor [B, K] (float32/float64, semiring domain).
+        retain: False (no trace), True (the trace backward() needs: rows of
+        unary sums may be left out and are filled by fill_trace() /
+        on first host access) or "full".
         Returns (outputs [B, R] tensor, values buffer [rows, ld])."""
         torch = _torch()
         if weights.dim() != 2 or weights.shape[1] != self.num_inputs:
@@ -287,15 +290,33 @@ class DevicePlan:
             outputs = torch.empty((B, self.num_roots), dtype=tdt, device=self.device)
         if workspace is None:
             workspace = self.forward_workspace(B, dtype)
+        mode = 0 if not retain else (1 if retain == "full" else _lib.KLAY_RETAIN_BACKWARD)
         rc = self._lib.klay_forward(
             self._handle, semiring, _klay_dtype(dtype), weights.data_ptr(), wdt,
-            values.data_ptr(), ld, 1 if retain else 0,
+            values.data_ptr(), ld, mode,
             outputs.data_ptr() if self.num_roots else None, B, float(epsilon),
             workspace.data_ptr() if workspace is not None else None, self._stream())
         _lib.check(rc, "klay_forward")
         # the trace's epsilon, for backward()'s unary-parent shortcut
         values.klay_epsilon = float(epsilon) if semiring == _lib.KLAY_LOG else -1.0
+        # a backward-only trace: complete it before reading rows on the host
+        values.klay_partial = (mode == _lib.KLAY_RETAIN_BACKWARD, B, semiring, float(epsilon))
         return outputs, values
+
+    def fill_trace(self, values, batch: int):
+        """Write the rows a backward-only trace left out (klay_fill_trace);
+        no-op for complete traces."""
+        partial = getattr(values, "klay_partial", None)
+        if not partial or not partial[0]:
+            return values
+        _, B, semiring, epsilon = partial
+        if values.dtype in (_torch().float32, _torch().float64):
+            dt = _lib.KLAY_F64 if values.dtype == _torch().float64 else _lib.KLAY_F32
+            rc = self._lib.klay_fill_trace(self._handle, semiring, dt, values.data_ptr(),
+                                           values.shape[1], B, epsilon, self._stream())
+            _lib.check(rc, "klay_fill_trace")
+        values.klay_partial = None
+        return values
 
     def capture(self, batch: int, dtype, semiring: int, epsilon: float = 0.0,
                 backward: bool = True, seeded: bool = False) -> "CapturedPass":
@@ -324,12 +345,18 @@ class DevicePlan:
             if tuple(seed.shape) != (batch, self.num_roots):
                 raise EvalError(f"seed must have shape {(batch, self.num_roots)}")
             seed = seed.to(device=self.device, dtype=tdt).contiguous()
+        if epsilon is None:
+            epsilon = getattr(values, "klay_epsilon", -1.0)
+        if domain != _lib.KLAY_LOG or epsilon != 0.0:
+            # this backward reads every row: complete a backward-only trace
+            self.fill_trace(values, batch)
+        partial = getattr(values, "klay_partial", None)
+        retain = _lib.KLAY_RETAIN_BACKWARD if partial and partial[0] else 1
         rc = self._lib.klay_backward(
             self._handle, domain, _klay_dtype(dtype), values.data_ptr(), values.shape[1],
             seed.data_ptr() if seed is not None else None,
             grads.data_ptr() if self.num_inputs else None, workspace.data_ptr(), batch,
-            float(epsilon if epsilon is not None else getattr(values, "klay_epsilon", -1.0)),
-            self._stream())
+            float(epsilon), retain, self._stream())
         _lib.check(rc, "klay_backward")
         return grads
 
@@ -425,6 +452,7 @@ class _NodeValues(Sequence):
         if not 0 <= l < len(self):
             raise IndexError(l)
         if l not in self._cache:
+            self._plan.fill_trace(self._values, self._batch)
             start = self._plan.layer_offsets[l]
             w = self._plan.num_inputs if l == 0 else self._plan.widths[l - 1]
             block = self._values[start:start + w, :self._batch]
