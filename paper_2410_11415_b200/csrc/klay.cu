@@ -481,8 +481,10 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       // backward child map
       d.alias_q = true;
       d.qa_e_base = (int64_t)aidx.size();
+      // (a unary node's child c sits W_P - c rows before the sum layer)
+      const int64_t wp = p->layers[l - 2].W;
       for (int64_t e = 0; e < E; ++e)
-        aidx.push_back(s_child[S[e]] >= 0 ? (int)(s_W + s_child[S[e]]) : (int)S[e]);
+        aidx.push_back(s_child[S[e]] >= 0 ? (int)(s_child[S[e]] - wp) : (int)S[e]);
       d.qb_map_base = (int64_t)omap.size();
       for (int64_t j = 0; j < s_W; ++j)
         omap.push_back(s_full[j] ? (s_child[j] | INT32_MIN) : (int)j);
@@ -704,11 +706,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       a.idx = p->d_aidx + d.fa.e_base;
       a.omap = p->d_omap + d.fa.map_base;
     }
-    if (alias_q) {
-      a.idx = p->d_aidx + d.qa_e_base;
-      a.prev2 = values + (size_t)p->layers[l - 2].row * ld;
-      a.nsplit = (int)p->layers[l - 1].W;
-    }
+    if (alias_q) a.idx = p->d_aidx + d.qa_e_base;  // negative rows: unary sums
     if (alias && d.mask_p) {
       a.mrow = p->d_omap + d.mrow_base;
       a.mbase = values + (size_t)p->layers[l + 1].row * ld;

@@ -37,8 +37,6 @@ struct LayerArgs {
   const int* omap;    // item node j -> output/own-value row; bit 31: alias output
                       // (backward pass-through: row of out2, masked by xalt)
   T* out2;            // alias outputs (adjoints of the layer two below)
-  const T* prev2;     // forward: operand rows >= nsplit live here (row - nsplit)
-  int nsplit;
   // forward of a product layer below an aliased sum layer: node j whose only
   // parent is a unary sum (row mrow[j] >= 0 of mbase, a row the forward
   // leaves unwritten) also stores there the finiteness bits of its value,

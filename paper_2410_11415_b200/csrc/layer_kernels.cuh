@@ -69,25 +69,21 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
   return x;
 }
 
-// ALIAS (log semiring, epsilon 0): operand rows >= nsplit are unary sums of
-// the layer below that the forward never wrote; they read their child's row
-// in prev2 instead, as logsumexp of one element (x, or NaN for +inf)
+// ALIAS (log semiring, epsilon 0): a negative operand row r is a unary sum
+// of the layer below that the forward never wrote; it reads its child's row
+// instead, r rows before the base (the child layer precedes the sum layer in
+// the trace), as the logsumexp of one element (the child, NaN for +inf)
 template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
   static constexpr bool ROWV = ALIAS, ALIAS_OUT = false;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 6)
   const T* base;
-  const T* base2;
   long long ld;
-  int nl, nsplit;
+  int nl;
   __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col, int nl_)
-      : base(a.prev + col), base2(ALIAS ? a.prev2 + col : nullptr), ld(a.ld), nl(nl_),
-        nsplit(a.nsplit) {}
-  __device__ __forceinline__ const T* row_ptr(int row) const {
-    if (ALIAS && row >= nsplit) return base2 + (size_t)(row - nsplit) * ld;
-    return base + (size_t)row * ld;
-  }
+      : base(a.prev + col), ld(a.ld), nl(nl_) {}
+  __device__ __forceinline__ const T* row_ptr(int row) const { return base + (long long)row * ld; }
   __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
     cp_async_vec(slot, lane, row_ptr(row), nl);
   }
@@ -95,11 +91,11 @@ struct FwdGather {
   __device__ __forceinline__ Vec<T> x_from_stage(const uint4*, int) const { return Vec<T>{}; }
   __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>&) const {
     const Vec<T> v = lds_vec<T>(slot, lane);
-    return (ALIAS && row >= nsplit) ? lse_unary(v) : v;
+    return (ALIAS && row < 0) ? lse_unary(v) : v;
   }
   __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>&) const {
     const Vec<T> v = ldv(row_ptr(row), nl);
-    return (ALIAS && row >= nsplit) ? lse_unary(v) : v;
+    return (ALIAS && row < 0) ? lse_unary(v) : v;
   }
   __device__ __forceinline__ Vec<T> load_x(int, int) const { return Vec<T>{}; }
 };
