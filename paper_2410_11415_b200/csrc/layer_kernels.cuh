@@ -114,7 +114,7 @@ struct BwdGather {
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
-                                                   : (MODE == BW_PASSA ? 3 : 1));  // (smem: 3)
+                                                   : (MODE == BW_PASSA ? KLAY_PASS_MINB : 1));
   const T* gbase;
   const T* nbase;
   const T* xbase;
