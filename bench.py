@@ -52,32 +52,95 @@ def load_peaks():
 # algorithmic bytes
 # ---------------------------------------------------------------------------
 
-def layer_bytes(tc, s, B, domain="log"):
-    """Per-launch algorithmic bytes of every forward and backward layer kernel.
-    fwd_l = s*B*(W_{l-1}+W_l) + 4*(E_l+W_l+1);
-    bwd_l = s*B*(2*W_{l-1} + W_l + P_l) + 4*(2E_l+W_{l-1}+1): parent
-    gradients (W_l rows) in, child values (W_{l-1}) in, child gradients
-    (W_{l-1}) out, plus P_l parent values: 0 for pass-through layers, W_l for
-    real-product layers, and for log-sum layers (epsilon 0) only the parents
-    with fan-in > 1 -- a unary parent's value is its child's own."""
+def _tail_from(tc):
+    """First layer of libklay's persistent tail (klay.cu: longest suffix of
+    layers with <= KLAY_TAIL_EDGES edges, at most 96 layers)."""
+    lim = int(os.environ.get("KLAY_TAIL_EDGES", "256"))
+    L = len(tc.layers)
+    t = L
+    while t > 0 and L - t < 96 and len(tc.layers[t - 1].sources) <= lim:
+        t -= 1
+    return t
+
+
+def layer_bytes(tc, s, B, domain="log", alias=None):
+    """Per-launch algorithmic bytes of every forward and backward layer kernel
+    (rows of s*B bytes; index bytes at 4 per entry).
+
+    Plain dataflow (reference order):
+      fwd_l = rows(W_{l-1} + W_l) + 4*(E_l + W_l + 1)
+      bwd_l = rows(2*W_{l-1} + W_l + P_l) + 4*(2E_l + W_{l-1} + 1): parent
+        adjoints (W_l) in, child values (W_{l-1}) in, child adjoints out,
+        plus P_l parent values: 0 for pass-through layers, W_l for real
+        products, the non-unary parents for log sums (epsilon 0).
+    With unary-sum aliases (log, epsilon 0, backward-only trace; klay.cu),
+    for an aliased sum layer S (U unary nodes, F of them the only parent of
+    their child) over product layer P, under product layer Q:
+      fwd S: the children of non-unary nodes in, W_S - U rows out
+      fwd P: + F finiteness masks (s*B/32 bytes each)
+      bwd Q: W_Q adjoints in, W_S rows out (to S or straight to P), F masks in
+      bwd S: kept children K = W_P - F: their parents' adjoints and non-unary
+             parents' values in, K child values in, K adjoints out.
+    """
+    if alias is None:
+        alias = domain == "log"
+    L = len(tc.layers)
+    tail = _tail_from(tc)
+    widths = [tc.num_inputs] + [l.width for l in tc.layers]
+    row = s * B
+    mask = s * B / 32.0
     fwd, bwd = {}, {}
+    info = {}
+    if alias:
+        for i in range(1, L - 1, 2):  # 0-based sum layers with a layer above
+            if i + 1 >= tail:
+                continue
+            lay = tc.layers[i]
+            seg = np.asarray(lay.segments)
+            src = np.asarray(lay.sources)
+            W, Wp = lay.width, widths[i]
+            fan = np.bincount(seg, minlength=W)
+            un_edge = fan[seg] == 1
+            gcnt = np.bincount(src, minlength=Wp)
+            full_child = np.zeros(Wp, bool)
+            full_child[src[un_edge]] = gcnt[src[un_edge]] == 1
+            kept = ~full_child
+            kept_edges = kept[src]
+            info[i] = dict(
+                U=int((fan == 1).sum()), F=int(full_child.sum()),
+                nu_children=int(np.unique(src[~un_edge]).size),
+                nu_edges=int((~un_edge).sum()),
+                K=int(kept.sum()),
+                K_edges=int(kept_edges.sum()),
+                K_parents=int(np.unique(seg[kept_edges]).size),
+                K_nu_parents=int(np.unique(seg[kept_edges & ~un_edge]).size))
     prev = tc.num_inputs
     for l, layer in enumerate(tc.layers, start=1):
+        i = l - 1
         W, E = layer.width, len(layer.sources)
-        fwd[l] = s * B * (prev + W) + 4 * (E + W + 1)
+        fwd[l] = row * (prev + W) + 4 * (E + W + 1)
         if domain == "log" and layer.op != "prod":
             P = int((np.bincount(np.asarray(layer.segments), minlength=W) > 1).sum())
-            bwd[l] = s * B * (2 * prev + W + P) + 4 * (2 * E + prev + 1)
+            bwd[l] = row * (2 * prev + W + P) + 4 * (2 * E + prev + 1)
         elif domain != "log" and layer.op == "prod":
-            bwd[l] = 2 * s * B * (prev + W) + 4 * (2 * E + prev + 1)
+            bwd[l] = 2 * row * (prev + W) + 4 * (2 * E + prev + 1)
         else:
-            bwd[l] = s * B * (prev + W) + 4 * (2 * E + prev + 1)
+            bwd[l] = row * (prev + W) + 4 * (2 * E + prev + 1)
+        if i in info:  # aliased sum layer S
+            d = info[i]
+            fwd[l] = row * (d["nu_children"] + W - d["U"]) + 4 * (d["nu_edges"] + 2 * (W - d["U"]) + 1)
+            bwd[l] = (row * (d["K_parents"] + d["K_nu_parents"] + 2 * d["K"])
+                      + 4 * (d["K_edges"] + 2 * d["K"] + 1))
+        if i + 1 in info:  # product layer P below an aliased S: masks out
+            fwd[l] += mask * info[i + 1]["F"] + 4 * W
+        if i - 1 in info:  # product layer Q above an aliased S
+            bwd[l] += mask * info[i - 1]["F"] + 4 * prev
         prev = W
     return fwd, bwd
 
 
-def bytes_per_eval(tc, s, B):
-    fwd, bwd = layer_bytes(tc, s, B)
+def bytes_per_eval(tc, s, B, alias=None):
+    fwd, bwd = layer_bytes(tc, s, B, alias=alias)
     return (sum(fwd.values()) + sum(bwd.values())) / B
 
 
