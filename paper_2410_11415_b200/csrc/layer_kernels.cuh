@@ -76,7 +76,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
-  static constexpr bool ROWV = ALIAS, ALIAS_OUT = false;
+  static constexpr bool ROWV = ALIAS, ALIAS_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 6)
   const T* base;
   long long ld;
@@ -109,7 +109,7 @@ struct BwdGather {
   static constexpr bool PASSLIKE = (MODE == BW_PASS || MODE == BW_PASSA);
   static constexpr int NOP = PASSLIKE ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
-  static constexpr bool ROWV = (NOP == 2), ALIAS_OUT = (MODE == BW_PASSA);
+  static constexpr bool ROWV = (NOP == 2), ALIAS_OUT = (MODE == BW_PASSA), ALIAS_IN = false;
   static constexpr int SE = 8;
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
@@ -450,15 +450,32 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
         auto val = [&](int e) {
           return g.value(st + e * EV, lane, G::ROWV ? widx[eb + e] : 0, x);
         };
-        Vec<T> out = val(sb);
+        Vec<T> out;
         if constexpr (RK == RK_SUM) {
           // x0 + (-0 + x1 + ... + x_{n-1}): n <= 8 keeps numpy's sequential branch
-          if (n > 1) {
-            Vec<T> acc = val(sb + 1);
-            for (int j = 2; j < n; ++j) acc = vadd(acc, val(sb + j));
-            out = vadd(out, acc);
+          auto sum = [&](auto&& v) {
+            Vec<T> o = v(sb);
+            if (n > 1) {
+              Vec<T> acc = v(sb + 1);
+              for (int j = 2; j < n; ++j) acc = vadd(acc, v(sb + j));
+              o = vadd(o, acc);
+            }
+            return o;
+          };
+          if constexpr (G::ALIAS_IN) {
+            // aliased operands (negative rows) read as logsumexp of one
+            // element: only a +inf one changes (to NaN), and then the plain
+            // sum is +inf or NaN -- redo the rare +inf results transformed
+            out = sum([&](int e) { return lds_vec<T>(st + e * EV, lane); });
+            bool redo = false;
+#pragma unroll
+            for (int c = 0; c < Vec<T>::N; ++c) redo |= (out.v[c] == T(INFINITY));
+            if (redo) out = sum([&](int e) { return g.value(st + e * EV, lane, widx[eb + e], x); });
+          } else {
+            out = sum(val);
           }
         } else if constexpr (RK == RK_LSE) {
+          out = val(sb);
           // a unary sum with epsilon 0 is an exact copy: log(exp(x - x) + 0) + x
           // == x, and -inf stays -inf (uniform branch: no exp/log issued)
           if (n > 1 || a.eps != T(0)) {
@@ -472,6 +489,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
             out = lse_unary(out);
           }
         } else {
+          out = val(sb);
           for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
         }
         const int id = nid(nd);
