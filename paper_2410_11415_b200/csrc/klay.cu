@@ -75,6 +75,14 @@ const bool g_no_tail = [] {
   return e && *e && *e != '0';
 }();
 
+// column-chunk order of consecutive layer kernels (klay::LayerArgs::rev):
+// 0 all first-to-last, 1 alternate per layer, 2 alternate per layer pair
+const int g_chunk_order = [] {
+  const char* e = getenv("KLAY_CHUNK_ORDER");
+  return (e && *e) ? atoi(e) : 1;
+}();
+int chunk_rev(int l) { return g_chunk_order == 1 ? (l & 1) : g_chunk_order == 2 ? ((l >> 1) & 1) : 0; }
+
 // KLAY_NO_ALIAS=1: every sum row is computed and read (A/B switch)
 const bool g_no_alias = [] {
   const char* e = getenv("KLAY_NO_ALIAS");
@@ -721,6 +729,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     a.out = cur;
     a.prev = prev;
     a.eps = (T)eps;
+    a.rev = chunk_rev(l);
     a.scratch = work;
     a.tpart = (long long)p->max_fslots * ld;
     if (l >= tail_from) {
@@ -814,6 +823,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
     a.unary_ok = (domain == SR_LOG_ && epsilon == 0.0) ? 1 : 0;
+    a.rev = chunk_rev(l + 1);
     a.hcount = (l >= tail_from) ? nullptr : hcount;
     if (l >= tail_from) {
       tail->layer[tail->n++] = a;

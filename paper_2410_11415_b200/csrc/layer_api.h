@@ -43,6 +43,7 @@ struct LayerArgs {
   // the only part of it the backward's alias outputs (PASSA) need
   const int* mrow;
   T* mbase;
+  int rev;            // visit the column chunks last to first (L2 reuse across launches)
 };
 
 // The persistent tail kernel (thin upper layers in one launch) takes its

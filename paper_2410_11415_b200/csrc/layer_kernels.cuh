@@ -644,7 +644,8 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
 #endif
   store_item_regs(ib, r, lane);
   __syncwarp();
-  run_item<T, RK, G>(a, ib, blockIdx.y, reinterpret_cast<uint4*>(wbase), lane);
+  run_item<T, RK, G>(a, ib, a.rev ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y,
+                     reinterpret_cast<uint4*>(wbase), lane);
 }
 
 // KLAY_NO_PDL=1 launches layer kernels fully serialized (A/B switch)
