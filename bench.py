@@ -345,7 +345,8 @@ def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / iters
     s = 8 if dtype == np.float64 else (1 / 8 if dtype == "u1" else 4)
-    fwd_b, bwd_b = layer_bytes(tc, s, B, semiring if semiring in ("log", "real") else "log")
+    fwd_b, bwd_b = layer_bytes(tc, s, B, semiring if semiring in ("log", "real") else "log",
+                               alias=(semiring == "log" and with_backward))
     alg = sum(fwd_b.values()) + (sum(bwd_b.values()) if with_backward else 0)
     peak, _ = load_peaks()
     nodes = tc.num_inputs + sum(l.width for l in tc.layers)

@@ -213,11 +213,10 @@ __device__ __forceinline__ void lse_merge(T& m, T& t, T m2, T t2) {
   if (m2 > m) {
     t = t * kexp(m - m2) + t2;
     m = m2;
-  } else if (isnan(m2)) {
-    m = m2;  // np.maximum.reduceat propagates NaN into the peak: the result is NaN
-    t = m2;
   } else if (m2 == -INFINITY) {
-    // contributes nothing (an all -inf part is masked to 0, engine.py:279)
+    // contributes nothing (an all -inf part is masked to 0, engine.py:279),
+    // except a NaN it saw (carried as a NaN sum)
+    if (isnan(t2)) t = t2;
   } else if (m2 == INFINITY) {
     // m == +inf too: every shifted term is masked to 0; only a NaN input
     // (carried as a NaN sum) must survive
@@ -260,11 +259,9 @@ struct LseOp {
       } else if (xv > m.v[c]) {
         t.v[c] = t.v[c] * kexp(m.v[c] - xv) + T(1);
         m.v[c] = xv;
-      } else if (isnan(xv)) {
-        m.v[c] = xv;  // the peak (np.maximum.reduceat) propagates NaN
-        t.v[c] = xv;
-      } else if (xv != T(-INFINITY) && xv != T(INFINITY)) {
-        // (xv == +inf here means m == +inf: exp(NaN) -> 0 in the reference)
+      } else if (fabs(xv) != T(INFINITY)) {
+        // (xv == +inf here means m == +inf: exp(NaN) -> 0 in the reference;
+        // a NaN xv makes the sum NaN, which result() turns into NaN)
         t.v[c] = t.v[c] + kexp(xv - m.v[c]);
       }
     }
@@ -279,7 +276,10 @@ struct LseOp {
       // a +inf peak shifts every element to exp(NaN or -inf) -> 0 in the
       // reference (engine.py:274-282): log(0 + eps) + inf = NaN, or +inf for eps > 0
       if (m.v[c] == T(INFINITY) && !isnan(t.v[c])) res = (eps > T(0)) ? T(INFINITY) : T(NAN);
-      r.v[c] = (m.v[c] == T(-INFINITY)) ? T(-INFINITY) : res;
+      // an all -inf segment stays -inf; a NaN element anywhere gives NaN (the
+      // reference's peak, np.maximum.reduceat, propagates it): a NaN after a
+      // -inf peak shows up as a NaN sum
+      r.v[c] = (m.v[c] == T(-INFINITY) && !isnan(t.v[c])) ? T(-INFINITY) : res;
     }
     return r;
   }
