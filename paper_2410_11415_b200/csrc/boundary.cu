@@ -111,8 +111,10 @@ void launch_seed(const T* seed, const int* top_off, const int* top_pos, T* g, in
   seed_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, top_off, top_pos, g, WL, R, B, ld);
 }
 
-// Rows of unary sum nodes a backward-only trace left unwritten: the child's
-// row as a logsumexp of one element (+inf -> NaN). One thread per element.
+// Rows of aliased (unary) nodes a backward-only trace left unwritten: the
+// source row {x & 0x7fffffff <- y}; bit 31 of x: the chain holds a unary sum,
+// so the value is a logsumexp of one element (+inf -> NaN). One thread per
+// element.
 template <typename T>
 __global__ void fill_aliases_kernel(const int2* __restrict__ pairs, long long n, T* values,
                                     long long ld) {
@@ -121,7 +123,7 @@ __global__ void fill_aliases_kernel(const int2* __restrict__ pairs, long long n,
   const long long k = i / ld, c = i - k * ld;
   const int2 pr = pairs[k];
   const T v = values[(size_t)pr.y * ld + c];
-  values[(size_t)pr.x * ld + c] = (v == T(INFINITY)) ? T(NAN) : v;
+  values[(size_t)(pr.x & 0x7fffffff) * ld + c] = (pr.x < 0 && v == T(INFINITY)) ? T(NAN) : v;
 }
 
 template <typename T>

@@ -229,7 +229,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
 
 // a compacted item set over a subset of a layer's nodes (unary-sum aliases)
 struct AliasSet {
-  int64_t off_base = 0, e_base = 0, map_base = 0;  // into aoff[] / aidx[] / omap[]
+  int64_t off_base = 0, e_base = 0, map_base = 0, xmap_base = 0;  // into aoff[] / aidx[] / omap[]
   int64_t i_base = 0, i_n = 0, h_base = 0, h_n = 0, slots = 0;
 };
 
@@ -243,24 +243,21 @@ struct LayerDesc {
   int64_t fi_base, fi_n, fh_base, fh_n, f_slots;  // forward items / heavy
   int64_t fq_base, fq_n;                           // forward items, no split (PROD)
   int64_t bi_base, bi_n, bh_base, bh_n, b_slots;  // backward items / heavy
-  // Unary-sum aliases (log semiring, epsilon 0). A sum node with one child
-  // has exactly its child's value (logsumexp of one element; +inf -> NaN),
-  // so with a backward-only trace (klay_forward retain = 2) such rows are
-  // never written:
-  //   alias_s  sum layer S: the forward computes only its non-unary nodes
-  //            (fa); the backward skips children whose only parent is unary
-  //            (ba), their adjoints come from the layer above
-  //   alias_q  product layer Q over S: forward operands of unary S nodes
-  //            read the child row two layers down (remapped sources, rows
-  //            >= W_S); the backward writes the adjoint of a unary S node
-  //            whose child has no other parent straight into that child's
-  //            row (omap bit 31), weighted by 1, or 0 for a non-finite child
-  //   mask_p   product layer P below an aliased S: its nodes whose only
-  //            parent is unary store their finiteness bits into that
-  //            parent's (unwritten) row, for the backward's alias weights
-  bool alias_s, alias_q, mask_p;
+  // Unary-node aliases (log semiring, epsilon 0, backward-only traces; see
+  // build_aliases). Per gate layer:
+  //   fa_on    forward runs over the non-aliased nodes only (compacted set fa)
+  //   fsrc_on  forward operands re-mapped: an aliased child reads its source
+  //            row (a negative offset from the layer's base); fsum_redo: a
+  //            product layer, whose aliased children are unary sums (+inf ->
+  //            NaN, redone only for +inf results)
+  //   mrow_on  nodes that are the target of a masked route store the
+  //            finiteness mask of their value in the route top's row
+  //   ba_on    backward over the children whose adjoint is not routed (ba),
+  //            absolute output rows (omap, bit 31: mask) and value rows (xmap)
+  //   bmask    some outputs need the mask (pass-through layers: PASSA)
+  bool fa_on, fsrc_on, fsum_redo, mrow_on, ba_on, bmask;
   AliasSet fa, ba;
-  int64_t qa_e_base, qb_map_base, mrow_base;
+  int64_t fsrc_base, mrow_base;
 };
 
 struct DeviceGuard {
@@ -341,6 +338,186 @@ static int upload(T** dst, const std::vector<T>& v) {
   return KLAY_OK;
 }
 
+// Unary-node aliases (LayerDesc). With the log semiring and epsilon 0 a gate
+// node with one child holds exactly its child's value: a product of one log
+// value is the value, a logsumexp of one is the value (+inf -> NaN). Every
+// such node below the tail (and not in the last layer) is "aliased": a
+// backward-only trace never writes its row, and readers use the row of the
+// chain's source, the first non-aliased node below. Adjoints flow down the
+// links "child with a single parent that is aliased" unchanged (products) or
+// weighted by 1 / 0 for a finite / non-finite value (sums); such a chain is a
+// route: the kernel computing the adjoint of the chain's top writes it
+// straight into the bottom's row, the nodes in between are never computed.
+// A route through a sum needs the value's finiteness mask: the bottom's
+// forward stores it into the top's (unwritten) value row.
+template <typename AddSet>
+static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const int64_t* sources,
+                          const int64_t* segments, const std::vector<int>& off,
+                          const std::vector<int>& toff, const std::vector<int>& tpar,
+                          std::vector<int>& aoff, std::vector<int>& aidx, std::vector<int>& omap,
+                          std::vector<int2>& pairs, AddSet add_set) {
+  const int L = p->L;
+  const int tail = p->tail_from;
+  auto width = [&](int nl) -> int64_t { return nl == 0 ? K : widths[nl - 1]; };
+  auto is_sum = [](int nl) { return nl >= 1 && ((nl - 1) % 2 == 1); };
+  std::vector<std::vector<int>> child(L + 1), npar(L + 1), par(L + 1), up(L + 1), srow(L + 1),
+      redirect(L + 1), mrow(L + 1);
+  std::vector<std::vector<char>> ali(L + 1), skip(L + 1), tf(L + 1);
+  for (int nl = 0; nl <= L; ++nl) {
+    const int64_t w = width(nl);
+    child[nl].assign(w, -1);
+    npar[nl].assign(w, 0);
+    par[nl].assign(w, -1);
+    up[nl].assign(w, -1);
+    srow[nl].resize(w);
+    redirect[nl].assign(w, -1);
+    mrow[nl].assign(w, -1);
+    ali[nl].assign(w, 0);
+    skip[nl].assign(w, 0);
+    tf[nl].assign(w, 0);
+    for (int64_t i = 0; i < w; ++i) srow[nl][i] = (int)(p->layer_row[nl] + i);
+  }
+  for (int l = 0; l < L; ++l) {
+    const LayerDesc& d = p->layers[l];
+    const int64_t* S = sources + d.e_base;
+    const int64_t* G = segments + d.e_base;
+    for (int64_t i = 0; i < d.W; ++i) {
+      const int c0 = off[d.off_base + i], c1 = off[d.off_base + i + 1];
+      if (c1 - c0 == 1) child[l + 1][i] = (int)S[c0];
+    }
+    for (int64_t e = 0; e < d.E; ++e) {
+      ++npar[l][S[e]];
+      par[l][S[e]] = (int)G[e];
+    }
+  }
+  // aliased nodes: unary, read by a regular (non-tail) kernel of the next layer
+  for (int nl = 1; nl < L && nl < tail; ++nl)
+    for (int64_t i = 0; i < width(nl); ++i) {
+      const int c = child[nl][i];
+      if (c < 0) continue;
+      ali[nl][i] = 1;
+      srow[nl][i] = srow[nl - 1][c];
+      tf[nl][i] = is_sum(nl) || tf[nl - 1][c];
+      pairs.push_back(make_int2((int)(p->layer_row[nl] + i) | (tf[nl][i] ? INT32_MIN : 0), srow[nl][i]));
+    }
+  // routes
+  static const int dbg_routes = [] {  // KLAY_ROUTES=0: none, 1: unmasked only (debug)
+    const char* e = getenv("KLAY_ROUTES");
+    return (e && *e) ? atoi(e) : 2;
+  }();
+  for (int nl = 0; nl < L && dbg_routes > 0; ++nl)
+    for (int64_t i = 0; i < width(nl); ++i)
+      if (npar[nl][i] == 1 && ali[nl + 1][par[nl][i]]) up[nl][i] = par[nl][i];
+  for (int nl = 0; nl < L; ++nl)
+    for (int64_t i = 0; i < width(nl); ++i) {
+      if (up[nl][i] < 0) continue;
+      if (ali[nl][i] && up[nl - 1][child[nl][i]] == (int)i) continue;  // inside a longer chain
+      int tl = nl, t = (int)i;
+      bool masked = false;
+      while (up[tl][t] >= 0) {
+        t = up[tl][t];
+        ++tl;
+        masked |= is_sum(tl);
+      }
+      // a masked route needs a computed bottom to write the mask
+      if (masked && (ali[nl][i] || nl == 0 || dbg_routes < 2)) continue;
+      if (dbg_routes >= 10 && tl - nl > dbg_routes - 10) continue;  // (debug: span limit)
+      for (int sl = nl, sj = (int)i; sl < tl; sj = up[sl][sj], ++sl) skip[sl][sj] = 1;
+      redirect[tl][t] = (int)(p->layer_row[nl] + i) | (masked ? INT32_MIN : 0);
+      if (masked) mrow[nl][i] = (int)(p->layer_row[tl] + t);
+    }
+  // per gate layer l (nodes: node layer l + 1, children: node layer l)
+  for (int l = 0; l < L; ++l) {
+    LayerDesc& d = p->layers[l];
+    const int nl = l + 1;
+    const int64_t W = d.W, Wp = d.Wprev;
+    const int64_t* S = sources + d.e_base;
+    auto operand = [&](int64_t c) -> int {
+      return ali[l][c] ? (int)(srow[l][c] - p->layer_row[l]) : (int)c;
+    };
+    bool any_child_ali = false, any_ali = false, any_mrow = false;
+    for (int64_t c = 0; c < Wp; ++c) any_child_ali |= ali[l][c] != 0;
+    for (int64_t i = 0; i < W; ++i) {
+      any_ali |= ali[nl][i] != 0;
+      any_mrow |= mrow[nl][i] >= 0;
+    }
+    if (any_child_ali) {
+      d.fsrc_on = true;
+      d.fsum_redo = d.prod;  // (the aliased children of a product layer are unary sums)
+      d.fsrc_base = (int64_t)aidx.size();
+      for (int64_t e = 0; e < d.E; ++e) aidx.push_back(operand(S[e]));
+    }
+    if (any_ali) {  // forward over the non-aliased nodes
+      d.fa_on = true;
+      ItemSet fa;
+      d.fa.off_base = (int64_t)aoff.size();
+      d.fa.e_base = (int64_t)aidx.size();
+      aoff.push_back(0);
+      int64_t nc = 0, ec = 0;
+      std::vector<int> ids, mr;
+      for (int64_t i = 0; i < W; ++i) {
+        if (ali[nl][i]) continue;
+        const int c0 = off[d.off_base + i], c1 = off[d.off_base + i + 1];
+        for (int e = c0; e < c1; ++e) aidx.push_back(operand(S[e]));
+        ec += c1 - c0;
+        aoff.push_back((int)ec);
+        ids.push_back((int)i);
+        mr.push_back(mrow[nl][i]);
+        ++nc;
+      }
+      d.fa.map_base = (int64_t)omap.size();
+      omap.insert(omap.end(), ids.begin(), ids.end());
+      d.fa.xmap_base = (int64_t)omap.size();
+      omap.insert(omap.end(), mr.begin(), mr.end());
+      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0);
+      add_set(fa, d.fa);
+      p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
+      p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)fa.heavy.size());
+    }
+    if (any_mrow) {
+      d.mrow_on = true;
+      d.mrow_base = (int64_t)omap.size();
+      omap.insert(omap.end(), mrow[nl].begin(), mrow[nl].end());
+    }
+    // backward over children whose adjoint is not routed
+    bool any_skip = false, any_top = false, any_masked = false;
+    for (int64_t c = 0; c < Wp; ++c) {
+      any_skip |= skip[l][c] != 0;
+      any_top |= redirect[l][c] != -1;  // (a masked redirect is negative: bit 31)
+      any_masked |= redirect[l][c] != -1 && (redirect[l][c] & INT32_MIN);
+    }
+    const bool logsum = !d.prod;  // (log domain: own values needed for the softmax weights)
+    if (any_skip || any_top || (logsum && any_child_ali)) {
+      d.ba_on = true;
+      d.bmask = !logsum && any_masked;
+      ItemSet ba;
+      d.ba.off_base = (int64_t)aoff.size();
+      d.ba.e_base = (int64_t)aidx.size();
+      aoff.push_back(0);
+      int64_t nc = 0, ec = 0;
+      std::vector<int> outs, xs;
+      for (int64_t c = 0; c < Wp; ++c) {
+        if (skip[l][c]) continue;
+        const int t0 = toff[d.toff_base + c], t1 = toff[d.toff_base + c + 1];
+        for (int t = t0; t < t1; ++t) aidx.push_back(tpar[d.e_base + t]);
+        ec += t1 - t0;
+        aoff.push_back((int)ec);
+        outs.push_back(redirect[l][c] != -1 ? redirect[l][c] : (int)(p->layer_row[l] + c));
+        xs.push_back(logsum ? srow[l][c] : (int)(p->layer_row[l] + c));
+        ++nc;
+      }
+      d.ba.map_base = (int64_t)omap.size();
+      omap.insert(omap.end(), outs.begin(), outs.end());
+      d.ba.xmap_base = (int64_t)omap.size();
+      omap.insert(omap.end(), xs.begin(), xs.end());
+      build_items(aoff, (size_t)d.ba.off_base, (int)nc, SHORT_BWD, ba, true, 0);
+      add_set(ba, d.ba);
+      p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
+      p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
+    }
+  }
+}
+
 extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const int64_t* widths,
                                 const int64_t* edge_counts, const int64_t* sources,
                                 const int64_t* segments, int32_t num_roots,
@@ -366,12 +543,6 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   std::vector<unsigned> masks;  // parallel to items
   std::vector<int> aoff, aidx, omap;
   std::vector<int2> alias_rows;
-  // the previous layer when it is an aliased sum layer: child of each unary
-  // node (-1 otherwise) and whether that child has no other parent
-  std::vector<int> s_child;
-  std::vector<char> s_full;
-  bool s_open = false;
-  int64_t s_W = 0;
   auto add_set = [&](ItemSet& set, AliasSet& as) {
     as.i_base = (int64_t)items.size();
     as.i_n = (int64_t)set.items.size();
@@ -483,81 +654,6 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.b_slots = bs.slots;
     p->max_fslots = std::max<int64_t>(p->max_fslots, fs.slots);
     p->max_bslots = std::max<int64_t>(p->max_bslots, bs.slots);
-    // ---- unary-sum aliases (see LayerDesc) ----
-    if (d.prod && s_open) {
-      // Q over the aliased sum layer below: remapped forward sources and the
-      // backward child map
-      d.alias_q = true;
-      d.qa_e_base = (int64_t)aidx.size();
-      // (a unary node's child c sits W_P - c rows before the sum layer)
-      const int64_t wp = p->layers[l - 2].W;
-      for (int64_t e = 0; e < E; ++e)
-        aidx.push_back(s_child[S[e]] >= 0 ? (int)(s_child[S[e]] - wp) : (int)S[e]);
-      d.qb_map_base = (int64_t)omap.size();
-      for (int64_t j = 0; j < s_W; ++j)
-        omap.push_back(s_full[j] ? (s_child[j] | INT32_MIN) : (int)j);
-    }
-    s_open = false;
-    if (!d.prod && l + 1 < num_layers && l + 1 < tail_from && W + prev_w < (1LL << 31)) {
-      d.alias_s = true;
-      s_child.assign(W, -1);
-      s_full.assign(W, 0);
-      for (int64_t i = 0; i < W; ++i) {
-        if (cnt[i] != 1) continue;
-        const int c = (int)S[off[d.off_base + i]];
-        s_child[i] = c;
-        s_full[i] = gcnt[c] == 1;
-        alias_rows.push_back(make_int2((int)(d.row + i), (int)(d.prev_row + c)));
-      }
-      // forward: the non-unary parents only
-      ItemSet fa, ba;
-      d.fa.off_base = (int64_t)aoff.size();
-      d.fa.e_base = (int64_t)aidx.size();
-      d.fa.map_base = (int64_t)omap.size();
-      aoff.push_back(0);
-      int64_t nc = 0, ec = 0;
-      for (int64_t i = 0; i < W; ++i) {
-        if (cnt[i] == 1) continue;
-        for (int e = off[d.off_base + i]; e < off[d.off_base + i + 1]; ++e) aidx.push_back((int)S[e]);
-        ec += cnt[i];
-        aoff.push_back((int)ec);
-        omap.push_back((int)i);
-        ++nc;
-      }
-      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0);
-      add_set(fa, d.fa);
-      // backward: children that are not the only child of a unary parent
-      d.ba.off_base = (int64_t)aoff.size();
-      d.ba.e_base = (int64_t)aidx.size();
-      d.ba.map_base = (int64_t)omap.size();
-      aoff.push_back(0);
-      nc = 0;
-      ec = 0;
-      for (int64_t j = 0; j < prev_w; ++j) {
-        const int t0 = toff[d.toff_base + j], t1 = toff[d.toff_base + j + 1];
-        if (t1 - t0 == 1 && cnt[tpar[tb + t0] & 0x7fffffff] == 1) continue;  // alias target
-        for (int t = t0; t < t1; ++t) aidx.push_back(tpar[tb + t]);
-        ec += t1 - t0;
-        aoff.push_back((int)ec);
-        omap.push_back((int)j);
-        ++nc;
-      }
-      build_items(aoff, (size_t)d.ba.off_base, (int)nc, SHORT_BWD, ba, true, 0);
-      add_set(ba, d.ba);
-      // the product layer below keeps the finiteness masks of alias targets
-      LayerDesc& dp = p->layers.back();
-      dp.mask_p = true;
-      dp.mrow_base = (int64_t)omap.size();
-      std::vector<int> mrow(prev_w, -1);
-      for (int64_t i = 0; i < W; ++i)
-        if (s_full[i]) mrow[s_child[i]] = (int)i;
-      omap.insert(omap.end(), mrow.begin(), mrow.end());
-      p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
-      p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
-      p->max_heavy = std::max<int64_t>(p->max_heavy, std::max(fa.heavy.size(), ba.heavy.size()));
-      s_open = true;
-      s_W = W;
-    }
     p->layers.push_back(d);
     p->layer_row.push_back(row);
     p->max_width = std::max(p->max_width, W);
@@ -567,6 +663,10 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   }
   p->total_rows = row;
   p->WL = prev_w;
+  if (num_layers >= 2 && row < (1LL << 30)) {
+    build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
+                  alias_rows, [&](ItemSet& set, AliasSet& as) { add_set(set, as); });
+  }
   p->n_alias = (int64_t)alias_rows.size();
 
   // roots (engine.py:203-212, 330-334)
@@ -640,7 +740,7 @@ extern "C" size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, in
 
 extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
   if (!plan) return 0;
-  return ((size_t)3 * plan->max_width + plan->max_bslots) * ld * esize(dtype) +
+  return ((size_t)plan->total_rows + plan->max_bslots) * ld * esize(dtype) +
          counter_bytes(plan, dtype, ld);
 }
 
@@ -702,9 +802,10 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
     LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
-    const bool alias_q = alias && d.alias_q;
-    if (alias && d.alias_s) {
-      // non-unary parents only (compacted CSR, node ids via omap)
+    const bool redo = alias && d.fsum_redo;
+    if (alias && d.fsrc_on) a.idx = p->d_aidx + d.fsrc_base;  // aliased children: source rows
+    if (alias && d.fa_on) {
+      // non-aliased nodes only (compacted CSR over re-mapped operands)
       a.items = p->d_items + d.fa.i_base;
       a.masks = p->d_masks + d.fa.i_base;
       a.n_items = (int)d.fa.i_n;
@@ -713,12 +814,11 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       a.off = p->d_aoff + d.fa.off_base;
       a.idx = p->d_aidx + d.fa.e_base;
       a.omap = p->d_omap + d.fa.map_base;
+      if (d.mrow_on) a.xmap = p->d_omap + d.fa.xmap_base;
+    } else if (alias && d.mrow_on) {
+      a.xmap = p->d_omap + d.mrow_base;
     }
-    if (alias_q) a.idx = p->d_aidx + d.qa_e_base;  // negative rows: unary sums
-    if (alias && d.mask_p) {
-      a.mrow = p->d_omap + d.mrow_base;
-      a.mbase = values + (size_t)p->layers[l + 1].row * ld;
-    }
+    if (alias && d.mrow_on) a.mbase = values;  // route masks (absolute rows)
     if (d.prod && (sr == SR_REAL_ || sr == KLAY_MAXPROD)) {
       // sequential product: heavy segments stay whole (no leaves, no combine)
       a.items = p->d_items + d.fq_base;
@@ -738,7 +838,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       a.hcount = hcount;
       LaunchScope ls(s, 0, l + 1);
       if constexpr (U1) g_launches += launch_forward_layer_u1(d.prod, a, s);
-      else g_launches += launch_forward_layer(sr, d.prod, alias_q, a, s);
+      else g_launches += launch_forward_layer(sr, d.prod, redo, a, s);
     }
     prev = cur;
   }
@@ -789,11 +889,10 @@ template <typename T>
 int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, const T* seed,
                   T* grads, T* work, int64_t B, double epsilon, int retain_mode, cudaStream_t s) {
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
-  // adjoints of node layer n (0 = inputs .. L) live in gb[n % 3]: a layer
-  // kernel reads layer l+1's and writes layer l's; alias outputs of a
-  // product layer go one further down, to layer l-1's
-  T* gb[3] = {work, work + (size_t)p->max_width * ld, work + (size_t)2 * p->max_width * ld};
-  T* scratch = work + (size_t)3 * p->max_width * ld;
+  // adjoints: one row per node, laid out like the trace (routes write rows
+  // of layers further down than the next)
+  T* gtrace = work;
+  T* scratch = work + (size_t)p->total_rows * ld;
   int* hcount = reinterpret_cast<int*>(scratch + (size_t)p->max_bslots * ld);
   if (p->max_heavy > 0) {
     const size_t nb = counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld);
@@ -801,7 +900,8 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   }
   {
     LaunchScope ls(s, 3, p->L + 1);
-    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, gb[p->L % 3], (int)p->WL, p->R, B, ld, s);
+    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, gtrace + (size_t)p->layer_row[p->L] * ld,
+                   (int)p->WL, p->R, B, ld, s);
     ++g_launches;
   }
   // alias outputs need the finiteness masks of a backward-only trace
@@ -817,8 +917,8 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
     LayerArgs<T> a = layer_args<T>(p, d, false, V, ld);
-    a.out = gb[l % 3];
-    a.gcur = gb[(l + 1) % 3];
+    a.out = gtrace + (size_t)d.prev_row * ld;
+    a.gcur = gtrace + (size_t)d.row * ld;
     a.ncur = trace + (size_t)d.row * ld;
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
@@ -855,8 +955,9 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       int mode = BW_PASS_;
       if (domain == SR_REAL_ && d.prod) mode = BW_REALPROD_;
       else if (domain == SR_LOG_ && !d.prod) mode = BW_LOGSUM_;
-      if (alias && d.alias_s) {
-        // children that are not the only child of a unary parent
+      if (alias && d.ba_on) {
+        // children whose adjoint is not routed; absolute output rows (route
+        // tops write their chain's bottom) and value rows
         a.items = p->d_items + d.ba.i_base;
         a.masks = p->d_masks + d.ba.i_base;
         a.n_items = (int)d.ba.i_n;
@@ -865,11 +966,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
         a.off = p->d_aoff + d.ba.off_base;
         a.idx = p->d_aidx + d.ba.e_base;
         a.omap = p->d_omap + d.ba.map_base;
-      }
-      if (alias && d.alias_q) {
-        mode = BW_PASSA_;
-        a.omap = p->d_omap + d.qb_map_base;
-        a.out2 = gb[(l - 1) % 3];
+        a.xmap = p->d_omap + d.ba.xmap_base;
+        a.out = gtrace;
+        a.nprev = trace;
+        if (d.bmask) mode = BW_PASSA_;
       }
       LaunchScope ls(s, 1, l + 1);
       g_launches += launch_backward_layer(mode, a, s);
@@ -877,7 +977,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   }
   if (p->K > 0) {
     LaunchScope ls(s, 3, 0);
-    launch_store_rows<T>(gb[0], grads, (int)p->K, B, ld, s);
+    launch_store_rows<T>(gtrace, grads, (int)p->K, B, ld, s);
     ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());

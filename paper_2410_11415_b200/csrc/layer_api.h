@@ -33,15 +33,16 @@ struct LayerArgs {
   int unary_ok;       // backward: edges flagged as unary parents need no parent value
   int* hcount;        // per (heavy segment, chunk) leaf counters: the last leaf combines
                       // (null: a separate combine pass / the tail's own barrier)
-  // unary-sum aliasing (klay.cu, "aliases"); all null/0 when off
-  const int* omap;    // item node j -> output/own-value row; bit 31: alias output
-                      // (backward pass-through: row of out2, masked by xalt)
-  T* out2;            // alias outputs (adjoints of the layer two below)
-  // forward of a product layer below an aliased sum layer: node j whose only
-  // parent is a unary sum (row mrow[j] >= 0 of mbase, a row the forward
-  // leaves unwritten) also stores there the finiteness bits of its value,
-  // the only part of it the backward's alias outputs (PASSA) need
-  const int* mrow;
+  // unary-node aliases (klay.cu build_aliases); all null when off
+  //   forward:  omap[j] = row of item node j (compacted sets); xmap[j] = row
+  //             of mbase where node j stores its value's finiteness mask, or
+  //             -1 (mbase null: no masks)
+  //   backward: omap[j] = output row (absolute; bit 31: weight the adjoint by
+  //             the value's finiteness), xmap[j] = own-value row (absolute):
+  //             the child's value (log-sum layers) or the row holding its
+  //             mask (pass-through layers)
+  const int* omap;
+  const int* xmap;
   T* mbase;
   int rev;            // visit the column chunks last to first (L2 reuse across launches)
 };

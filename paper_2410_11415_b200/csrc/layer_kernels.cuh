@@ -76,7 +76,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
-  static constexpr bool ROWV = ALIAS, ALIAS_OUT = false, ALIAS_IN = ALIAS;
+  static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 6)
   const T* base;
   long long ld;
@@ -100,16 +100,16 @@ struct FwdGather {
   __device__ __forceinline__ Vec<T> load_x(int, int) const { return Vec<T>{}; }
 };
 
-// PASSA: pass-through whose children may be alias outputs (omap bit 31): the
-// adjoint of a unary sum goes straight to its only child, two layers down,
-// with the unary softmax weight: 1, or 0 for a non-finite child value, read
-// from the finiteness mask the forward left in the unary sum's own row
+// PASSA: pass-through whose outputs may carry a route's unary weight (omap
+// bit 31): 1, or 0 for a non-finite value, read from the finiteness mask the
+// forward left in the route top's unwritten row (xmap)
 template <typename T, int MODE>
 struct BwdGather {
   static constexpr bool PASSLIKE = (MODE == BW_PASS || MODE == BW_PASSA);
   static constexpr int NOP = PASSLIKE ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
-  static constexpr bool ROWV = (NOP == 2), ALIAS_OUT = (MODE == BW_PASSA), ALIAS_IN = false;
+  // (outputs flagged in omap carry the unary weight: own value or mask needed)
+  static constexpr bool ROWV = (NOP == 2), MASKED_OUT = (NX == 1), ALIAS_IN = false;
   static constexpr int SE = 8;
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
@@ -140,23 +140,24 @@ struct BwdGather {
     if constexpr (NOP == 2)
       if (!unary_edge(row)) cp_async_vec(slot + NV * 32, lane, nbase + r * ld, nl);
   }
-  // own value of node id `node` (item node `j`). PASSA: alias outputs only,
-  // as the finiteness mask in child row j (see store_mask)
-  __device__ __forceinline__ void issue_x(uint4* slot, int node, int j, int lane) const {
+  // own value of an output (omap entry `out`, value row `xrow`). PASSA:
+  // flagged outputs only, as the finiteness mask at the chunk's start
+  __device__ __forceinline__ void issue_x(uint4* slot, int out, int xrow, int lane) const {
     if (MODE == BW_PASSA) {
-      if (node < 0 && lane < NV)
-        cp_async16(slot + lane, xbase + (size_t)j * ld + lane * (16 / sizeof(T)));
+      if (out < 0 && lane < NV)
+        cp_async16(slot + lane, xbase + (size_t)xrow * ld + lane * (16 / sizeof(T)));
     } else {
-      cp_async_vec(slot, lane, xbase + (size_t)node * ld, nl);
+      cp_async_vec(slot, lane, xbase + (size_t)xrow * ld, nl);
     }
   }
   __device__ __forceinline__ Vec<T> x_from_stage(const uint4* slot, int lane) const {
     if (MODE == BW_PASSA) return mask_to_x<T>(reinterpret_cast<const unsigned*>(slot), lane);
     return lds_vec<T>(slot, lane);
   }
-  __device__ __forceinline__ Vec<T> load_x(int node, int j) const {
+  __device__ __forceinline__ Vec<T> load_x(int out, int xrow) const {
     if (MODE == BW_PASSA) {
-      if (node >= 0) return Vec<T>{};
+      if (out >= 0) return Vec<T>{};
+      const int j = xrow;
       unsigned w[NV * 4];
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
@@ -165,7 +166,7 @@ struct BwdGather {
       }
       return mask_to_x<T>(w, (int)(threadIdx.x & 31));
     }
-    return ldv(xbase + (size_t)node * ld, nl);
+    return ldv(xbase + (size_t)xrow * ld, nl);
   }
   __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>& x) const {
     if constexpr (NOP == 2) {
@@ -279,7 +280,8 @@ struct ItemIndex {
   int pad[3];
   int widx[TASK_EDGES];
   int woff[32];       // short task: segment offsets relative to it.z
-  int wmap[32];       // with LayerArgs::omap: node ids of the item's nodes
+  int wmap[32];       // LayerArgs::omap entries of the item's nodes
+  int wxmap[32];      // LayerArgs::xmap entries
 };
 
 template <typename T, typename G>
@@ -323,7 +325,7 @@ struct ItemRegs {
   unsigned mask;
   int idx[TASK_EDGES / 32];
   int off;
-  int map;
+  int map, xmap;
 };
 
 // index loads of one item whose descriptor (it, mask) is already known
@@ -341,8 +343,9 @@ __device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int4 i
   }
   const int nn = r.it.y - r.it.x;
   r.off = (r.it.y > 0 && lane <= nn) ? __ldg(a.off + r.it.x + lane) - r.it.z : 0;
-  const int* mp = a.omap ? a.omap : a.mrow;  // (never both)
-  r.map = (mp && lane < (r.it.y > 0 ? nn : 1)) ? __ldg(mp + r.it.x + lane) : 0;
+  const bool in = lane < (r.it.y > 0 ? nn : 1);
+  r.map = (a.omap && in) ? __ldg(a.omap + r.it.x + lane) : 0;
+  r.xmap = (a.xmap && in) ? __ldg(a.xmap + r.it.x + lane) : 0;
   return r;
 }
 
@@ -360,6 +363,7 @@ __device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r
   for (int q = 0; q < TASK_EDGES / 32; ++q) ib->widx[q * 32 + lane] = r.idx[q];
   ib->woff[lane] = r.off;
   ib->wmap[lane] = r.map;
+  ib->wxmap[lane] = r.xmap;
 }
 
 // Run one item (index data in `ib`, synchronized) for one 512-byte column
@@ -392,6 +396,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   const int* widx = ib->widx;
   const int* woff = ib->woff;
   const int* wmap = ib->wmap;
+  const int* wxmap = ib->wxmap;
 
   // Lanes (pieces) past the row work on valid columns and never store: the
   // whole warp runs the same instruction stream without divergence.
@@ -413,6 +418,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     // node id of item node nd: output row / own-value row (omap: compacted
     // item sets and alias outputs, see LayerArgs)
     auto nid = [&](int nd) { return a.omap ? wmap[nd] : nb + nd; };
+    auto xid = [&](int nd) { return a.xmap ? wxmap[nd] : nb + nd; };
     const size_t col0 = (size_t)chunk * 32 * NV * PIECE<T>;  // the chunk's first column
     unsigned m_issue = ib->mask, m_scan = ib->mask;
     auto next_batch = [&](unsigned& m, int& n0, int& n1) {
@@ -427,7 +433,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       const int eb = woff[n0], cnt = woff[n1] - eb;
       for (int i = 0; i < cnt; ++i) g.issue(st + i * EV, widx[eb + i], lane);
       if constexpr (G::NX)
-        for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nid(nd), nb + nd, lane);
+        for (int nd = n0; nd < n1; ++nd) g.issue_x(st + SE * EV + (nd - n0) * XV, nid(nd), xid(nd), lane);
       cp_async_commit();
     };
     const int nbat = __popc(ib->mask);
@@ -493,15 +499,12 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
           for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, val(sb + j));
         }
         const int id = nid(nd);
-        if constexpr (G::ALIAS_OUT) {
-          if (id < 0) {
-            stv(a.out2 + (size_t)(id & 0x7fffffff) * ld + col, G::unary(out, x), na);
-            continue;
-          }
+        if constexpr (G::MASKED_OUT) {
+          if (id < 0) out = G::unary(out, x);
         }
-        stv(a.out + (size_t)id * ld + col, out, na);
-        if (a.mrow) {
-          const int mr = wmap[nd];
+        stv(a.out + (size_t)(id & 0x7fffffff) * ld + col, out, na);
+        if (a.mbase) {
+          const int mr = wxmap[nd];
           if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + col0, out, lane);
         }
       }
@@ -511,11 +514,12 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
 
   // ===================== long segment / leaf =====================
   const bool leaf = it.y < 0;
-  const int node = a.omap ? wmap[0] : it.x;  // node id (see the short path; wmap = mrow otherwise)
+  const int node = a.omap ? wmap[0] : it.x;  // output (see the short path)
+  const int xnode = a.xmap ? wxmap[0] : it.x;
   const int t0 = leaf ? 0 : 1;      // first tail edge (relative)
   const int m = ne - t0;            // tail length
   Vec<T> x{};
-  if constexpr (G::NX) x = g.load_x(node, it.x);
+  if constexpr (G::NX) x = g.load_x(node, xnode);
   auto row_of = [&](int e) { return staged_idx ? widx[e] : __ldg(a.idx + it.z + e); };
   // round t stages tail elements [8t, 8t+8)
   auto issue = [&](int t) {
@@ -610,18 +614,14 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     if constexpr (RK == RK_SUM) out = (m == 0) ? x0 : vadd(x0, res);
     else if constexpr (RK == RK_LSE) out = lse.result();
     else out = acc;
-    if (a.mrow) {  // (all lanes: ballots)
-      const int mr = wmap[0];
-      if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + (size_t)chunk * 32 * NV * PIECE<T>, out, lane);
+    if (a.mbase) {  // (all lanes: ballots)
+      if (xnode >= 0) store_mask(a.mbase + (size_t)xnode * ld + (size_t)chunk * 32 * NV * PIECE<T>, out, lane);
     }
     if (na == 0) return;
-    if constexpr (G::ALIAS_OUT) {
-      if (node < 0) {
-        stv(a.out2 + (size_t)(node & 0x7fffffff) * ld + col, G::unary(out, x), na);
-        return;
-      }
+    if constexpr (G::MASKED_OUT) {
+      if (node < 0) out = G::unary(out, x);
     }
-    stv(a.out + (size_t)node * ld + col, out, na);
+    stv(a.out + (size_t)(node & 0x7fffffff) * ld + col, out, na);
   }
 }
 
@@ -673,9 +673,10 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
   const int node = hv.x, slot0 = hv.y, nleaf = hv.z;
   const int s = __ldg(a.off + node);
   const int n = __ldg(a.off + node + 1) - s;
-  const int id = a.omap ? __ldg(a.omap + node) : node;  // output / own-value row
+  const int id = a.omap ? __ldg(a.omap + node) : node;    // output row
+  const int xid = a.xmap ? __ldg(a.xmap + node) : node;  // own-value / mask row
   const G g(a, col, nl);
-  const Vec<T> x = g.load_x(id, node);
+  const Vec<T> x = g.load_x(id, xid);
   const Vec<T> x0 = g.direct(__ldg(a.idx + s), x);
   Vec<T> res;
   if constexpr (RK == RK_SUM) {
@@ -709,17 +710,13 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
     for (int l = 0; l < nleaf; ++l) op.push(ldv(a.scratch + (size_t)(slot0 + l) * ld + col, nl));
     res = op.result();
   }
-  if (a.mrow) {
-    const int mr = __ldg(a.mrow + node);
-    if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + (size_t)chunk * 32 * NV * PIECE<T>, res, lane);
+  if (a.mbase) {
+    if (xid >= 0) store_mask(a.mbase + (size_t)xid * ld + (size_t)chunk * 32 * NV * PIECE<T>, res, lane);
   }
-  if constexpr (G::ALIAS_OUT) {
-    if (id < 0) {
-      stv(a.out2 + (size_t)(id & 0x7fffffff) * ld + col, G::unary(res, x), lc.na);
-      return;
-    }
+  if constexpr (G::MASKED_OUT) {
+    if (id < 0) res = G::unary(res, x);
   }
-  stv(a.out + (size_t)id * ld + col, res, lc.na);
+  stv(a.out + (size_t)(id & 0x7fffffff) * ld + col, res, lc.na);
 }
 
 constexpr int COMBINE_LEAVES = 64;  // leaf partials staged per combine warp
