@@ -29,6 +29,10 @@ constexpr int TASK_EDGES_H = 64;   // edges per short task (<= TASK_EDGES)
 constexpr int TASK_NODES_H = 31;   // nodes per short task (<= TASK_NODES)
 constexpr int SHORT_FWD = 8;       // FwdGather::SE
 constexpr int SHORT_BWD = 8;       // BwdGather::SE
+#ifndef KLAY_LOGSUM_SE
+#define KLAY_LOGSUM_SE 4
+#endif
+constexpr int SHORT_BWD_SUM = KLAY_LOGSUM_SE;  // BwdGather<LOGSUM>::SE (sum layers)
 constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are split
 // persistent tail (layer_kernels.cuh tail_kernel): the suffix of layers with
 // at most TAIL_EDGES edges runs in one launch per direction
@@ -510,7 +514,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       omap.insert(omap.end(), outs.begin(), outs.end());
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
-      build_items(aoff, (size_t)d.ba.off_base, (int)nc, SHORT_BWD, ba, true, 0);
+      build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : SHORT_BWD_SUM, ba, true, 0);
       add_set(ba, d.ba);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
@@ -624,7 +628,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
                                                    (TAIL_CLUSTER * TAIL_WARPS_H) + 7) & ~7))
         : 0;
     build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap);
-    build_items(toff, (size_t)d.toff_base, (int)prev_w, SHORT_BWD, bs, true, tcap);
+    build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : SHORT_BWD_SUM, bs, true, tcap);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());

@@ -24,6 +24,9 @@ constexpr int WARPS_PER_BLOCK = 4;
 #ifndef KLAY_FWD_MINB
 #define KLAY_FWD_MINB 6
 #endif
+#ifndef KLAY_LOGSUM_SE
+#define KLAY_LOGSUM_SE 4
+#endif
 #ifndef KLAY_LOGSUM_MINB
 #define KLAY_LOGSUM_MINB 1
 #endif
@@ -110,7 +113,9 @@ struct BwdGather {
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   // (outputs flagged in omap carry the unary weight: own value or mask needed)
   static constexpr bool ROWV = (NOP == 2), MASKED_OUT = (NX == 1), ALIAS_IN = false;
-  static constexpr int SE = 8;
+  // edges per stage batch: log-sum layers stage three rows per edge and are
+  // shared-memory bound, so they use 4 (their segments are short)
+  static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : 8;
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
@@ -522,8 +527,11 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   if constexpr (G::NX) x = g.load_x(node, xnode);
   auto row_of = [&](int e) { return staged_idx ? widx[e] : __ldg(a.idx + it.z + e); };
   // round t stages tail elements [8t, 8t+8)
+  // rounds of 8 are double-buffered when a stage holds 8 edges; policies
+  // with smaller stages (SE < 8) use both stages as one 8-edge buffer
+  constexpr bool DB = SE >= 8;
   auto issue = [&](int t) {
-    uint4* st = stage + (t & 1) * STAGE_V;
+    uint4* st = DB ? stage + (t & 1) * STAGE_V : stage;
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
     const int my_row = (lane < cnt) ? row_of(base + lane) : 0;
@@ -545,13 +553,13 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     if (!leaf) lse.push(x0);
   }
   for (int t = 0; t < nr; ++t) {
-    if (t + 1 < nr) {
+    if (DB && t + 1 < nr) {
       issue(t + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    const uint4* st = stage + (t & 1) * STAGE_V;
+    const uint4* st = DB ? stage + (t & 1) * STAGE_V : stage;
     const int base = t0 + 8 * t;
     const int cnt = min(8, ne - base);
     auto val = [&](int i) {
@@ -576,6 +584,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       if (leaf && t == 0) acc = val(i++);
       for (; i < cnt; ++i) seq_combine<T, RK>(acc, val(i));
     }
+    if (!DB && t + 1 < nr) issue(t + 1);  // (each lane reuses only its own slots)
   }
   if constexpr (RK == RK_SUM) {
     if (m >= 8 && mainend == m) res = combine8(r);
