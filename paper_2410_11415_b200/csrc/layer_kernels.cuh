@@ -28,7 +28,7 @@ constexpr int WARPS_PER_BLOCK = 4;
 #define KLAY_LOGSUM_SE 4
 #endif
 #ifndef KLAY_LOGSUM_MINB
-#define KLAY_LOGSUM_MINB 1
+#define KLAY_LOGSUM_MINB 4
 #endif
 
 
