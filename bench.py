@@ -63,6 +63,75 @@ def _tail_from(tc):
     return t
 
 
+_ALIAS_PLANS = {}
+
+
+def alias_plan(tc):
+    key = (id(tc), _tail_from(tc))
+    if key not in _ALIAS_PLANS:
+        _ALIAS_PLANS[key] = _alias_plan(tc)
+    return _ALIAS_PLANS[key]
+
+
+def _alias_plan(tc):
+    """Host restatement of libklay's unary-node aliases and adjoint routes
+    (klay.cu build_aliases), for the byte model: per node layer, which nodes
+    are aliased, their source row, and which adjoints are routed."""
+    L = len(tc.layers)
+    tail = _tail_from(tc)
+    widths = [tc.num_inputs] + [l.width for l in tc.layers]
+    rows = np.cumsum([0] + widths)
+    child, npar, par, ali, srow = [], [], [], [], []
+    for nl in range(L + 1):
+        w = widths[nl]
+        child.append(np.full(w, -1))
+        npar.append(np.zeros(w, np.int64))
+        par.append(np.full(w, -1))
+        ali.append(np.zeros(w, bool))
+        srow.append(rows[nl] + np.arange(w))
+    for l, lay in enumerate(tc.layers):
+        seg, src = np.asarray(lay.segments), np.asarray(lay.sources)
+        fan = np.bincount(seg, minlength=lay.width)
+        un = fan[seg] == 1
+        child[l + 1][seg[un]] = src[un]
+        npar[l] += np.bincount(src, minlength=widths[l])
+        par[l][src] = seg
+    is_sum = lambda nl: nl >= 1 and (nl - 1) % 2 == 1
+    for nl in range(1, min(L, tail)):
+        m = child[nl] >= 0
+        ali[nl] = m
+        srow[nl][m] = srow[nl - 1][child[nl][m]]
+    up = [np.where((npar[nl] == 1) & (par[nl] >= 0), par[nl], -1) for nl in range(L)]
+    for nl in range(L):
+        ok = up[nl] >= 0
+        ok[ok] = ali[nl + 1][up[nl][ok]]
+        up[nl] = np.where(ok, up[nl], -1)
+    up.append(np.full(widths[L], -1))
+    skip = [np.zeros(w, bool) for w in widths]
+    top = [np.zeros(w, bool) for w in widths]
+    masked_top = [np.zeros(w, bool) for w in widths]
+    mask_src = [np.zeros(w, bool) for w in widths]
+    for nl in range(L):
+        for i in np.nonzero(up[nl] >= 0)[0]:
+            if ali[nl][i] and up[nl - 1][child[nl][i]] == i:
+                continue
+            tl, t, masked, path = nl, i, False, [(nl, i)]
+            while up[tl][t] >= 0:
+                t = up[tl][t]
+                tl += 1
+                masked |= is_sum(tl)
+                path.append((tl, t))
+            if masked and (ali[nl][i] or nl == 0):
+                continue
+            for a, b in path[:-1]:
+                skip[a][b] = True
+            top[tl][t] = True
+            masked_top[tl][t] = masked
+            mask_src[nl][i] = masked
+    return dict(widths=widths, ali=ali, srow=srow, skip=skip, masked_top=masked_top,
+                mask_src=mask_src, tail=tail)
+
+
 def layer_bytes(tc, s, B, domain="log", alias=None):
     """Per-launch algorithmic bytes of every forward and backward layer kernel
     (rows of s*B bytes; index bytes at 4 per entry).
@@ -73,68 +142,56 @@ def layer_bytes(tc, s, B, domain="log", alias=None):
         adjoints (W_l) in, child values (W_{l-1}) in, child adjoints out,
         plus P_l parent values: 0 for pass-through layers, W_l for real
         products, the non-unary parents for log sums (epsilon 0).
-    With unary-sum aliases (log, epsilon 0, backward-only trace; klay.cu),
-    for an aliased sum layer S (U unary nodes, F of them the only parent of
-    their child) over product layer P, under product layer Q:
-      fwd S: the children of non-unary nodes in, W_S - U rows out
-      fwd P: + F finiteness masks (s*B/32 bytes each)
-      bwd Q: W_Q adjoints in, W_S rows out (to S or straight to P), F masks in
-      bwd S: kept children K = W_P - F: their parents' adjoints and non-unary
-             parents' values in, K child values in, K adjoints out.
+    With unary-node aliases and adjoint routes (log, epsilon 0,
+    backward-only trace; klay.cu build_aliases, restated in alias_plan):
+      fwd_l = rows(distinct operand rows of the computed nodes + computed
+        nodes) + masks (s*B/32 bytes per route bottom) + indices
+      bwd_l = rows(distinct parents of the computed children (adjoints)
+        + their non-unary parents (values, log sums) + distinct own-value
+        rows (log sums) + computed children) + masks of masked route tops
+        (pass-through layers) + indices
     """
     if alias is None:
         alias = domain == "log"
-    L = len(tc.layers)
-    tail = _tail_from(tc)
-    widths = [tc.num_inputs] + [l.width for l in tc.layers]
     row = s * B
     mask = s * B / 32.0
     fwd, bwd = {}, {}
-    info = {}
-    if alias:
-        for i in range(1, L - 1, 2):  # 0-based sum layers with a layer above
-            if i + 1 >= tail:
-                continue
-            lay = tc.layers[i]
-            seg = np.asarray(lay.segments)
-            src = np.asarray(lay.sources)
-            W, Wp = lay.width, widths[i]
-            fan = np.bincount(seg, minlength=W)
-            un_edge = fan[seg] == 1
-            gcnt = np.bincount(src, minlength=Wp)
-            full_child = np.zeros(Wp, bool)
-            full_child[src[un_edge]] = gcnt[src[un_edge]] == 1
-            kept = ~full_child
-            kept_edges = kept[src]
-            info[i] = dict(
-                U=int((fan == 1).sum()), F=int(full_child.sum()),
-                nu_children=int(np.unique(src[~un_edge]).size),
-                nu_edges=int((~un_edge).sum()),
-                K=int(kept.sum()),
-                K_edges=int(kept_edges.sum()),
-                K_parents=int(np.unique(seg[kept_edges]).size),
-                K_nu_parents=int(np.unique(seg[kept_edges & ~un_edge]).size))
+    ap = alias_plan(tc) if alias else None
     prev = tc.num_inputs
     for l, layer in enumerate(tc.layers, start=1):
         i = l - 1
         W, E = layer.width, len(layer.sources)
-        fwd[l] = row * (prev + W) + 4 * (E + W + 1)
-        if domain == "log" and layer.op != "prod":
-            P = int((np.bincount(np.asarray(layer.segments), minlength=W) > 1).sum())
-            bwd[l] = row * (2 * prev + W + P) + 4 * (2 * E + prev + 1)
-        elif domain != "log" and layer.op == "prod":
-            bwd[l] = 2 * row * (prev + W) + 4 * (2 * E + prev + 1)
+        seg, src = np.asarray(layer.segments), np.asarray(layer.sources)
+        fan = np.bincount(seg, minlength=W)
+        if ap is None:
+            fwd[l] = row * (prev + W) + 4 * (E + W + 1)
+            if domain == "log" and layer.op != "prod":
+                P = int((fan > 1).sum())
+                bwd[l] = row * (2 * prev + W + P) + 4 * (2 * E + prev + 1)
+            elif domain != "log" and layer.op == "prod":
+                bwd[l] = 2 * row * (prev + W) + 4 * (2 * E + prev + 1)
+            else:
+                bwd[l] = row * (prev + W) + 4 * (2 * E + prev + 1)
+            prev = W
+            continue
+        ali_n, ali_c = ap["ali"][l], ap["ali"][i]
+        src_rows = ap["srow"][i][src]
+        comp = ~ali_n[seg]                      # edges of computed nodes
+        n_comp = int((~ali_n).sum())
+        fwd[l] = (row * (np.unique(src_rows[comp]).size + n_comp)
+                  + mask * int(ap["mask_src"][l].sum()) + 4 * (int(comp.sum()) + 2 * n_comp + 1))
+        kept = ~ap["skip"][i]
+        ke = kept[src]                          # edges of computed children
+        n_kept = int(kept.sum())
+        adj = np.unique(seg[ke]).size
+        if layer.op == "prod":
+            bwd[l] = (row * (adj + n_kept) + mask * int(ap["masked_top"][i].sum())
+                      + 4 * (2 * int(ke.sum()) + 2 * n_kept + 1))
         else:
-            bwd[l] = row * (prev + W) + 4 * (2 * E + prev + 1)
-        if i in info:  # aliased sum layer S
-            d = info[i]
-            fwd[l] = row * (d["nu_children"] + W - d["U"]) + 4 * (d["nu_edges"] + 2 * (W - d["U"]) + 1)
-            bwd[l] = (row * (d["K_parents"] + d["K_nu_parents"] + 2 * d["K"])
-                      + 4 * (d["K_edges"] + 2 * d["K"] + 1))
-        if i + 1 in info:  # product layer P below an aliased S: masks out
-            fwd[l] += mask * info[i + 1]["F"] + 4 * W
-        if i - 1 in info:  # product layer Q above an aliased S
-            bwd[l] += mask * info[i - 1]["F"] + 4 * prev
+            nonun = ke & (fan[seg] > 1)
+            bwd[l] = (row * (adj + np.unique(seg[nonun]).size
+                             + np.unique(ap["srow"][i][kept]).size + n_kept)
+                      + 4 * (2 * int(ke.sum()) + 3 * n_kept + 1))
         prev = W
     return fwd, bwd
 
