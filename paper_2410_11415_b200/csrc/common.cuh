@@ -114,9 +114,18 @@ __device__ __forceinline__ Vec<T> vadd(const Vec<T>& a, const Vec<T>& b) {
   return r;
 }
 
+// fp32 exp / log on the SFU (ex2.approx / lg2.approx: ~2^-22 relative,
+// special values as expf / logf; subnormal results flush to 0). The log
+// semiring's fp32 tolerance (rel 1e-5 vs the fp64 reference) holds with
+// margin; KLAY_PRECISE_F32 selects the libm versions. fp64 stays exact.
+#ifdef KLAY_PRECISE_F32
 __device__ __forceinline__ float kexp(float x) { return expf(x); }
-__device__ __forceinline__ double kexp(double x) { return exp(x); }
 __device__ __forceinline__ float klog(float x) { return logf(x); }
+#else
+__device__ __forceinline__ float kexp(float x) { return __expf(x); }
+__device__ __forceinline__ float klog(float x) { return __logf(x); }
+#endif
+__device__ __forceinline__ double kexp(double x) { return exp(x); }
 __device__ __forceinline__ double klog(double x) { return log(x); }
 
 // np.maximum / np.minimum: NaN-propagating.
