@@ -26,7 +26,10 @@ enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2, BW_PASSA = 3 };
 enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4, RK_AND = 5, RK_OR = 6 };
 
 // numpy's pairwise summation works on blocks of at most this many elements
-constexpr int PW_BLOCK = 128;
+#ifndef KLAY_PW_BLOCK
+#define KLAY_PW_BLOCK 128
+#endif
+constexpr int PW_BLOCK = KLAY_PW_BLOCK;  // numpy pairwise block (128; other values: experiments only)
 
 #ifndef KLAY_NV
 #define KLAY_NV 1

@@ -33,7 +33,10 @@ constexpr int SHORT_BWD = 8;       // BwdGather::SE
 #define KLAY_LOGSUM_SE 4
 #endif
 constexpr int SHORT_BWD_SUM = KLAY_LOGSUM_SE;  // BwdGather<LOGSUM>::SE (sum layers)
-constexpr int PW_BLOCK_H = 128;    // numpy pairwise block; longer tails are split
+#ifndef KLAY_PW_BLOCK
+#define KLAY_PW_BLOCK 128
+#endif
+constexpr int PW_BLOCK_H = KLAY_PW_BLOCK;  // numpy pairwise block; longer tails are split
 // persistent tail (layer_kernels.cuh tail_kernel): the suffix of layers with
 // at most TAIL_EDGES edges runs in one launch per direction
 const int TAIL_EDGES = [] {

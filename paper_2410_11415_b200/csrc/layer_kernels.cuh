@@ -17,7 +17,10 @@
 
 namespace klay {
 
-constexpr int WARPS_PER_BLOCK = 4;
+#ifndef KLAY_WARPS_PER_BLOCK
+#define KLAY_WARPS_PER_BLOCK 4
+#endif
+constexpr int WARPS_PER_BLOCK = KLAY_WARPS_PER_BLOCK;
 #ifndef KLAY_PASS_MINB
 #define KLAY_PASS_MINB 5  // resident blocks of the pass-through backward kernel
 #endif
