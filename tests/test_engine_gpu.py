@@ -408,3 +408,36 @@ def test_log_domain_nonfinite_inputs_match_oracle(cuda, name, eps):
     nv = _NodeValues(plan, vals, B)
     for l in range(len(tr)):
         rel_close(nv[l], tr[l], 1e-12, 1e-12)
+
+
+@pytest.mark.parametrize("name", ["fig_main", "rnnf_wide", "A", "B", "C", "E", "Cp"])
+def test_backward_only_trace_matches_full_trace(cuda, name):
+    """retain=2 (unary nodes aliased: never written, adjoints routed down
+    chains; klay.cu build_aliases) against retain=1 (every row written, plain
+    backward): after klay_fill_trace the traces are bitwise equal, and the
+    gradients of the two backward paths are bitwise equal, also with
+    non-finite inputs."""
+    import torch
+    from paper_2410_11415_b200 import _lib, device_plan
+    tc, gold = (load_config if name in CONFIGS else load_case)(name)
+    plan = device_plan(tc)
+    rng = np.random.default_rng(3)
+    B = 40
+    lw = np.log(rng.uniform(0.05, 0.95, size=(B, tc.num_inputs)))
+    lw[rng.uniform(size=lw.shape) < 0.05] = -np.inf
+    lw[rng.uniform(size=lw.shape) < 0.01] = np.inf
+    lw[rng.uniform(size=lw.shape) < 0.01] = np.nan
+    lw[: B // 2] = np.log(rng.uniform(0.05, 0.95, size=(B // 2, tc.num_inputs)))
+    for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+        x = torch.tensor(lw, dtype=tdt, device=cuda)
+        out_p, vals_p = plan.forward(x, _lib.KLAY_LOG, dt)                  # backward-only
+        out_f, vals_f = plan.forward(x, _lib.KLAY_LOG, dt, retain="full")   # every row
+        assert torch.equal(out_p.nan_to_num(), out_f.nan_to_num())
+        g_p = plan.backward(vals_p, B, _lib.KLAY_LOG, dt)   # aliases + routes
+        g_f = plan.backward(vals_f, B, _lib.KLAY_LOG, dt)   # plain
+        assert torch.equal(torch.isnan(g_p), torch.isnan(g_f))
+        assert torch.equal(g_p.nan_to_num(), g_f.nan_to_num())
+        plan.fill_trace(vals_p, B)
+        a, b = vals_p[:, :B], vals_f[:, :B]
+        assert torch.equal(torch.isnan(a), torch.isnan(b))
+        assert torch.equal(a.nan_to_num(), b.nan_to_num())
