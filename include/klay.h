@@ -106,9 +106,10 @@ KLAY_API int64_t klay_row_stride(int64_t batch, int32_t dtype);
  *                2 * max_width rows (ping-pong, only the last layer survives)
  *   retain       0: no trace; 1: full trace; 2 (KLAY_RETAIN_BACKWARD): the
  *                trace klay_backward needs. With KLAY_LOG and epsilon 0 the
- *                rows of unary sum nodes (a copy of their only child) are
- *                then left unwritten: neither layer above nor klay_backward
- *                reads them. klay_fill_trace() writes them on demand.
+ *                rows of unary gate nodes below the tail (each a copy of its
+ *                only child, +inf -> NaN through a sum) are then left
+ *                unwritten: readers use the first non-unary row below.
+ *                klay_fill_trace() writes them on demand.
  *   outputs      device [B, R] row-major, element type `dtype` (may be NULL)
  *   epsilon      log semiring only, added inside the log (must be >= 0)
  *   workspace    device scratch of klay_forward_workspace() bytes (may be
@@ -122,9 +123,9 @@ KLAY_API int klay_forward(const KlayPlan* plan, int32_t semiring, int32_t dtype,
 #define KLAY_RETAIN_BACKWARD 2
 
 /* Completes a retain = 2 trace of klay_forward(semiring, epsilon): writes the
- * rows of unary sum nodes from their children (logsumexp of one element: the
- * child, NaN for +inf). No-op for traces that left nothing out (any
- * semiring but KLAY_LOG, epsilon != 0). */
+ * rows of unary nodes from their chains' sources (through a unary sum, a
+ * logsumexp of one element: +inf becomes NaN). No-op for traces that left
+ * nothing out (any semiring but KLAY_LOG, epsilon != 0). */
 KLAY_API int klay_fill_trace(const KlayPlan* plan, int32_t semiring, int32_t dtype, void* values,
                     int64_t ld, int64_t batch, double epsilon, void* stream);
 
@@ -147,9 +148,9 @@ KLAY_API size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, int6
  *                other value, e.g. -1 when unknown, reads every parent.
  *   retain       the retain mode klay_forward wrote the trace with (1 full,
  *                2 backward-only). A backward-only log trace with epsilon 0
- *                carries, in the rows of unary sums, the finiteness masks
- *                this backward uses to send their adjoints straight to
- *                their children; pass 1 for any other (e.g. uploaded) trace.
+ *                carries, in unwritten rows, the finiteness masks this
+ *                backward uses to send adjoints down chains of unary nodes
+ *                in one step; pass 1 for any other (e.g. uploaded) trace.
  */
 KLAY_API int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, const void* trace,
                   int64_t ld, const void* seed, void* grads, void* workspace,

@@ -267,7 +267,7 @@ class DevicePlan:
                 values=None, outputs=None, workspace=None):
         """weights: cuda tensor [B, K] (float32/float64, semiring domain).
         retain: False (no trace), True (the trace backward() needs: rows of
-        unary sums may be left out and are filled by fill_trace() /
+        unary nodes may be left out and are filled by fill_trace() /
         on first host access) or "full".
         Returns (outputs [B, R] tensor, values buffer [rows, ld])."""
         torch = _torch()
