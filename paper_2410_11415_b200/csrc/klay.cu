@@ -25,8 +25,14 @@ enum { SR_REAL_ = 0, SR_LOG_ = 1 };
 enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2, BW_PASSA_ = 3 };
 
 // work-item shape (see layer_kernels.cuh)
-constexpr int TASK_EDGES_H = 64;   // edges per short task (<= TASK_EDGES)
-constexpr int TASK_NODES_H = 31;   // nodes per short task (<= TASK_NODES)
+#ifndef KLAY_TASK_EDGES
+#define KLAY_TASK_EDGES 32
+#endif
+constexpr int TASK_EDGES_H = KLAY_TASK_EDGES;  // edges per short task (<= TASK_EDGES)
+#ifndef KLAY_TASK_NODES
+#define KLAY_TASK_NODES 16
+#endif
+constexpr int TASK_NODES_H = KLAY_TASK_NODES;  // nodes per short task (<= TASK_NODES)
 constexpr int SHORT_FWD = 8;       // FwdGather::SE
 constexpr int SHORT_BWD = 8;       // BwdGather::SE
 #ifndef KLAY_LOGSUM_SE
