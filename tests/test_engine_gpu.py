@@ -9,6 +9,7 @@ gradient scale, because grads near zero carry absolute error).
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -441,3 +442,21 @@ def test_backward_only_trace_matches_full_trace(cuda, name):
         a, b = vals_p[:, :B], vals_f[:, :B]
         assert torch.equal(torch.isnan(a), torch.isnan(b))
         assert torch.equal(a.nan_to_num(), b.nan_to_num())
+
+
+@pytest.mark.parametrize("tail_edges", ["0", "100000"])
+def test_alias_and_tail_extremes(cuda, tail_edges):
+    """The persistent tail normally takes every small circuit whole (no
+    aliases there). Re-run the golden, non-finite and trace-equality suites
+    with no tail (every unary node below the last layer aliased, routes
+    everywhere) and with an all-tail schedule (KLAY_TAIL_EDGES is read when
+    libklay loads, hence the subprocess)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, KLAY_TAIL_EDGES=tail_edges)
+    r = subprocess.run(
+        [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+         os.path.join(os.path.dirname(__file__), "test_engine_gpu.py"),
+         "-k", "golden_small or nonfinite or backward_only or consumer"],
+        env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
