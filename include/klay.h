@@ -158,6 +158,26 @@ KLAY_API int klay_backward(const KlayPlan* plan, int32_t domain, int32_t dtype, 
 
 KLAY_API size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld);
 
+/* ---- .klay reader ---------------------------------- */
+
+/*
+ * Parse and validate `.klay` text (tensorize.py:197-313; the structural rules
+ * of tensorize.py:94-132). Rejects, never repairs: KLAY_EFORMAT with the
+ * reason in klay_read_klay_error(). Host only (no CUDA).
+ *   sizes[7] from klay_file_info: num_inputs, num_vars, num_layers,
+ *   num_edges, num_roots, num_constant_roots, inputmap entries.
+ * Layer ops alternate product (layer 1) / sum, as validated.
+ */
+typedef struct KlayFile KlayFile;
+KLAY_API int klay_read_klay(const char* text, int64_t len, KlayFile** out);
+KLAY_API const char* klay_read_klay_error(void);
+KLAY_API int klay_file_info(const KlayFile* file, int64_t* sizes);
+KLAY_API int klay_file_export(const KlayFile* file, int64_t* widths, int64_t* counts,
+                     int64_t* sources, int64_t* segments, int64_t* roots,
+                     int64_t* const_pos, int64_t* const_val, int64_t* lit_codes,
+                     int64_t* lit_slots);
+KLAY_API void klay_file_destroy(KlayFile* file);
+
 /* ---- host-side layerization ----------------------- */
 
 /*

@@ -41,6 +41,11 @@ SIGNATURES = {
     "klay_backward_workspace": (ctypes.c_size_t, [_vp, _c_i32, _c_i64]),
     "klay_fill_trace": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i64, _c_i64, ctypes.c_double,
                                         _vp]),
+    "klay_read_klay": (ctypes.c_int, [ctypes.c_char_p, _c_i64, ctypes.POINTER(_vp)]),
+    "klay_read_klay_error": (ctypes.c_char_p, []),
+    "klay_file_info": (ctypes.c_int, [_vp, _vp]),
+    "klay_file_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "klay_file_destroy": (None, [_vp]),
     "klay_layerize": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      ctypes.POINTER(_vp)]),
     "klay_layered_info": (_c_i64, [_vp, _c_i32]),

@@ -98,9 +98,42 @@ BAD = {
 
 @pytest.mark.parametrize("case", sorted(BAD))
 def test_read_klay_rejects(case):
-    from paper_2410_11415_b200.tensorized import KlayFormatError, read_klay
+    from paper_2410_11415_b200.tensorized import KlayFormatError, read_klay, read_klay_py
     with pytest.raises(KlayFormatError):
-        read_klay(BAD[case])
+        read_klay(BAD[case])     # libklay's C++ reader
+    with pytest.raises(KlayFormatError):
+        read_klay_py(BAD[case])  # the Python reader
+
+
+def _accepts(reader, text):
+    from paper_2410_11415_b200.tensorized import KlayFormatError
+    try:
+        return reader(text)
+    except KlayFormatError:
+        return None
+
+
+@pytest.mark.parametrize("name", ["fig_main", "corpus_3", "rnnf_small", "constants", "dup_child"])
+def test_native_and_python_klay_readers_agree(name):
+    """Round trips are equal, and randomly corrupted files are accepted or
+    rejected alike (and parse to the same circuit when accepted)."""
+    from paper_2410_11415_b200.tensorized import read_klay, read_klay_py, write_klay
+    tc, _ = load_case(name)
+    buf = io.StringIO()
+    write_klay(tc, buf)
+    text = buf.getvalue()
+    assert read_klay(text) == read_klay_py(text) == tc
+    rng = np.random.default_rng(5)
+    toks = text.split(" ")
+    for _ in range(150):
+        t = list(toks)
+        k = int(rng.integers(len(t)))
+        t[k] = str(rng.choice(["0", "1", "-1", "7", "x", "", "2:1", "1:0", "99999"]))
+        bad = " ".join(t)
+        a, b = _accepts(read_klay, bad), _accepts(read_klay_py, bad)
+        assert (a is None) == (b is None), (k, t[k])
+        if a is not None:
+            assert a == b
 
 
 def test_weight_constructors_match_reference_semantics():
