@@ -34,6 +34,7 @@ constexpr int TASK_EDGES_H = KLAY_TASK_EDGES;  // edges per short task (<= TASK_
 #endif
 constexpr int TASK_NODES_H = KLAY_TASK_NODES;  // nodes per short task (<= TASK_NODES)
 constexpr int SHORT_FWD = 8;       // FwdGather::SE
+constexpr int PADW_H = 32;         // padded per-item index data (klay::PADW)
 constexpr int SHORT_BWD = 8;       // BwdGather::SE
 #ifndef KLAY_LOGSUM_SE
 #define KLAY_LOGSUM_SE 4
@@ -244,6 +245,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
 struct AliasSet {
   int64_t off_base = 0, e_base = 0, map_base = 0, xmap_base = 0;  // into aoff[] / aidx[] / omap[]
   int64_t i_base = 0, i_n = 0, h_base = 0, h_n = 0, slots = 0;
+  int64_t pmap_base = -1, pxmap_base = -1;  // padded per-item maps (pmap[] / pxmap[])
 };
 
 struct LayerDesc {
@@ -258,19 +260,18 @@ struct LayerDesc {
   int64_t bi_base, bi_n, bh_base, bh_n, b_slots;  // backward items / heavy
   // Unary-node aliases (log semiring, epsilon 0, backward-only traces; see
   // build_aliases). Per gate layer:
-  //   fa_on    forward runs over the non-aliased nodes only (compacted set fa)
-  //   fsrc_on  forward operands re-mapped: an aliased child reads its source
-  //            row (a negative offset from the layer's base); fsum_redo: a
-  //            product layer, whose aliased children are unary sums (+inf ->
-  //            NaN, redone only for +inf results)
+  //   fa_on    forward runs over its own item set fa: the non-aliased nodes,
+  //            operands re-mapped (an aliased child reads its source row, a
+  //            negative offset from the layer's base); fsum_redo: a product
+  //            layer whose aliased children are unary sums (+inf -> NaN,
+  //            redone only for +inf results)
   //   mrow_on  nodes that are the target of a masked route store the
   //            finiteness mask of their value in the route top's row
   //   ba_on    backward over the children whose adjoint is not routed (ba),
   //            absolute output rows (omap, bit 31: mask) and value rows (xmap)
   //   bmask    some outputs need the mask (pass-through layers: PASSA)
-  bool fa_on, fsrc_on, fsum_redo, mrow_on, ba_on, bmask;
+  bool fa_on, fsum_redo, mrow_on, ba_on, bmask;
   AliasSet fa, ba;
-  int64_t fsrc_base, mrow_base;
 };
 
 struct DeviceGuard {
@@ -313,7 +314,11 @@ struct KlayPlan {
   int* d_aoff = nullptr;   // unary-sum aliases: compacted offsets,
   int* d_aidx = nullptr;   // compacted / remapped edge indices,
   int* d_omap = nullptr;   // item node -> node id maps
-  int2* d_alias = nullptr;  // {trace row of a unary sum, trace row of its child}
+  int2* d_alias = nullptr;  // {trace row of an aliased node (bit 31: via a sum), source row}
+  int* d_pidx = nullptr;   // padded per-item edge indices / offsets (parallel to d_items)
+  int* d_poff = nullptr;
+  int* d_pmap = nullptr;   // padded per-item maps of alias sets (omap, xmap)
+  int* d_pmap2 = nullptr;
   int64_t n_alias = 0;
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
   int32_t tail_from = 0;  // first layer of the persistent tail (L = no tail)
@@ -340,6 +345,10 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_aidx);
   cudaFree(p->d_omap);
   cudaFree(p->d_alias);
+  cudaFree(p->d_pidx);
+  cudaFree(p->d_poff);
+  cudaFree(p->d_pmap);
+  cudaFree(p->d_pmap2);
   delete p;
 }
 
@@ -454,13 +463,10 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       any_ali |= ali[nl][i] != 0;
       any_mrow |= mrow[nl][i] >= 0;
     }
-    if (any_child_ali) {
-      d.fsrc_on = true;
-      d.fsum_redo = d.prod;  // (the aliased children of a product layer are unary sums)
-      d.fsrc_base = (int64_t)aidx.size();
-      for (int64_t e = 0; e < d.E; ++e) aidx.push_back(operand(S[e]));
-    }
-    if (any_ali) {  // forward over the non-aliased nodes
+    d.fsum_redo = d.prod && any_child_ali;  // (a product layer's aliased children are unary sums)
+    if (any_child_ali || any_ali || any_mrow) {
+      // own forward item set: the computed nodes, operands at source rows,
+      // node ids (compacted) and mask rows
       d.fa_on = true;
       ItemSet fa;
       d.fa.off_base = (int64_t)aoff.size();
@@ -478,19 +484,15 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
         mr.push_back(mrow[nl][i]);
         ++nc;
       }
-      d.fa.map_base = (int64_t)omap.size();
-      omap.insert(omap.end(), ids.begin(), ids.end());
-      d.fa.xmap_base = (int64_t)omap.size();
-      omap.insert(omap.end(), mr.begin(), mr.end());
+      d.fa.map_base = any_ali ? (int64_t)omap.size() : -1;  // (-1: identity)
+      if (any_ali) omap.insert(omap.end(), ids.begin(), ids.end());
+      d.fa.xmap_base = any_mrow ? (int64_t)omap.size() : -1;
+      if (any_mrow) omap.insert(omap.end(), mr.begin(), mr.end());
+      d.mrow_on = any_mrow;
       build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0);
-      add_set(fa, d.fa);
+      add_set(fa, d.fa, aoff, (size_t)d.fa.off_base, aidx, (size_t)d.fa.e_base);
       p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)fa.heavy.size());
-    }
-    if (any_mrow) {
-      d.mrow_on = true;
-      d.mrow_base = (int64_t)omap.size();
-      omap.insert(omap.end(), mrow[nl].begin(), mrow[nl].end());
     }
     // backward over children whose adjoint is not routed
     bool any_skip = false, any_top = false, any_masked = false;
@@ -524,7 +526,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
       build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : SHORT_BWD_SUM, ba, true, 0);
-      add_set(ba, d.ba);
+      add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
     }
@@ -556,11 +558,39 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   std::vector<unsigned> masks;  // parallel to items
   std::vector<int> aoff, aidx, omap;
   std::vector<int2> alias_rows;
-  auto add_set = [&](ItemSet& set, AliasSet& as) {
+  // Padded per-item index data (PADW ints per item, parallel to items[]):
+  // the edge indices of items with <= PADW edges and the raw segment offsets
+  // of short tasks, so a warp fetches an item's structure in one round trip
+  // instead of descriptor-then-indices (klay::item_regs_from).
+  std::vector<int> pidx, poff, pmap, pxmap;
+  auto pad_items = [&](const std::vector<int4>& its, const std::vector<int>& ov, size_t ob,
+                       const std::vector<int>& iv, size_t ib) {
+    for (const int4& it : its) {
+      const int ne = it.w - it.z, nn = it.y > 0 ? it.y - it.x : -1;
+      for (int j = 0; j < PADW_H; ++j) {
+        pidx.push_back(ne <= PADW_H && j < ne ? iv[ib + it.z + j] : 0);
+        poff.push_back(j <= nn ? ov[ob + it.x + j] : 0);
+      }
+    }
+  };
+  auto pad_maps = [&](const std::vector<int4>& its, std::vector<int>& dst, int64_t base) -> int64_t {
+    if (base < 0) return -1;
+    const int64_t at = (int64_t)dst.size();
+    for (const int4& it : its) {
+      const int nn = it.y > 0 ? it.y - it.x : 1;
+      for (int j = 0; j < PADW_H; ++j) dst.push_back(j < nn ? omap[(size_t)base + it.x + j] : 0);
+    }
+    return at;
+  };
+  auto add_set = [&](ItemSet& set, AliasSet& as, const std::vector<int>& ov, size_t ob,
+                     const std::vector<int>& iv, size_t ib) {
     as.i_base = (int64_t)items.size();
     as.i_n = (int64_t)set.items.size();
     items.insert(items.end(), set.items.begin(), set.items.end());
     masks.insert(masks.end(), set.masks.begin(), set.masks.end());
+    pad_items(set.items, ov, ob, iv, ib);
+    as.pmap_base = pad_maps(set.items, pmap, as.map_base);
+    as.pxmap_base = pad_maps(set.items, pxmap, as.xmap_base);
     as.h_base = (int64_t)heavy.size();
     as.h_n = (int64_t)set.heavy.size();
     heavy.insert(heavy.end(), set.heavy.begin(), set.heavy.end());
@@ -642,6 +672,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
     masks.insert(masks.end(), fs.masks.begin(), fs.masks.end());
+    pad_items(fs.items, off, (size_t)d.off_base, src, (size_t)d.e_base);
     d.fq_base = d.fi_base;
     d.fq_n = d.fi_n;
     if (d.prod && !fs.heavy.empty()) {
@@ -651,11 +682,13 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       d.fq_n = (int64_t)qs.items.size();
       items.insert(items.end(), qs.items.begin(), qs.items.end());
       masks.insert(masks.end(), qs.masks.begin(), qs.masks.end());
+      pad_items(qs.items, off, (size_t)d.off_base, src, (size_t)d.e_base);
     }
     d.bi_base = (int64_t)items.size();
     d.bi_n = (int64_t)bs.items.size();
     items.insert(items.end(), bs.items.begin(), bs.items.end());
     masks.insert(masks.end(), bs.masks.begin(), bs.masks.end());
+    pad_items(bs.items, toff, (size_t)d.toff_base, tpar, (size_t)d.e_base);
     d.fh_base = (int64_t)heavy.size();
     d.fh_n = (int64_t)fs.heavy.size();
     p->max_heavy = std::max<int64_t>(p->max_heavy, std::max(fs.heavy.size(), bs.heavy.size()));
@@ -678,7 +711,9 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   p->WL = prev_w;
   if (num_layers >= 2 && row < (1LL << 30)) {
     build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
-                  alias_rows, [&](ItemSet& set, AliasSet& as) { add_set(set, as); });
+                  alias_rows,
+                  [&](ItemSet& set, AliasSet& as, const std::vector<int>& ov, size_t ob,
+                      const std::vector<int>& iv, size_t ib) { add_set(set, as, ov, ob, iv, ib); });
   }
   p->n_alias = (int64_t)alias_rows.size();
 
@@ -708,7 +743,9 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       (rc = upload(&p->d_root_node, rn)) || (rc = upload(&p->d_const, cv)) ||
       (rc = upload(&p->d_top_off, top_off)) || (rc = upload(&p->d_top_pos, top_pos)) ||
       (rc = upload(&p->d_aoff, aoff)) || (rc = upload(&p->d_aidx, aidx)) ||
-      (rc = upload(&p->d_omap, omap)) || (rc = upload(&p->d_alias, alias_rows))) {
+      (rc = upload(&p->d_omap, omap)) || (rc = upload(&p->d_alias, alias_rows)) ||
+      (rc = upload(&p->d_pidx, pidx)) || (rc = upload(&p->d_poff, poff)) ||
+      (rc = upload(&p->d_pmap, pmap)) || (rc = upload(&p->d_pmap2, pxmap))) {
     plan_free(p);
     return rc;
   }
@@ -759,6 +796,20 @@ extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, i
 
 namespace {
 
+// point a layer's arguments at an alias item set (items, heavy, padded data)
+template <typename T>
+void set_items(LayerArgs<T>& a, const KlayPlan* p, const AliasSet& as) {
+  a.items = p->d_items + as.i_base;
+  a.masks = p->d_masks + as.i_base;
+  a.n_items = (int)as.i_n;
+  a.heavy = p->d_heavy + as.h_base;
+  a.n_heavy = (int)as.h_n;
+  a.pidx = p->d_pidx + (size_t)as.i_base * PADW_H;
+  a.poff = p->d_poff + (size_t)as.i_base * PADW_H;
+  a.pmap = as.pmap_base >= 0 ? p->d_pmap + as.pmap_base : nullptr;
+  a.pxmap = as.pxmap_base >= 0 ? p->d_pmap2 + as.pxmap_base : nullptr;
+}
+
 template <typename T>
 LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, int64_t ld) {
   LayerArgs<T> a{};
@@ -768,6 +819,8 @@ LayerArgs<T> layer_args(const KlayPlan* p, const LayerDesc& d, bool fwd, int V, 
   a.heavy = p->d_heavy + (fwd ? d.fh_base : d.bh_base);
   a.n_heavy = (int)(fwd ? d.fh_n : d.bh_n);
   a.off = fwd ? p->d_off + d.off_base : p->d_toff + d.toff_base;
+  a.pidx = p->d_pidx + (size_t)(fwd ? d.fi_base : d.bi_base) * PADW_H;
+  a.poff = p->d_poff + (size_t)(fwd ? d.fi_base : d.bi_base) * PADW_H;
   a.idx = fwd ? p->d_src + d.e_base : p->d_tpar + d.e_base;
   a.V = V;
   a.ld = ld;
@@ -816,26 +869,21 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
     LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
     const bool redo = alias && d.fsum_redo;
-    if (alias && d.fsrc_on) a.idx = p->d_aidx + d.fsrc_base;  // aliased children: source rows
     if (alias && d.fa_on) {
-      // non-aliased nodes only (compacted CSR over re-mapped operands)
-      a.items = p->d_items + d.fa.i_base;
-      a.masks = p->d_masks + d.fa.i_base;
-      a.n_items = (int)d.fa.i_n;
-      a.heavy = p->d_heavy + d.fa.h_base;
-      a.n_heavy = (int)d.fa.h_n;
+      // the layer's own set: non-aliased nodes over re-mapped operands
+      set_items(a, p, d.fa);
       a.off = p->d_aoff + d.fa.off_base;
       a.idx = p->d_aidx + d.fa.e_base;
-      a.omap = p->d_omap + d.fa.map_base;
-      if (d.mrow_on) a.xmap = p->d_omap + d.fa.xmap_base;
-    } else if (alias && d.mrow_on) {
-      a.xmap = p->d_omap + d.mrow_base;
+      if (d.fa.map_base >= 0) a.omap = p->d_omap + d.fa.map_base;
+      if (d.fa.xmap_base >= 0) a.xmap = p->d_omap + d.fa.xmap_base;
+      if (d.mrow_on) a.mbase = values;  // route masks (absolute rows)
     }
-    if (alias && d.mrow_on) a.mbase = values;  // route masks (absolute rows)
     if (d.prod && (sr == SR_REAL_ || sr == KLAY_MAXPROD)) {
       // sequential product: heavy segments stay whole (no leaves, no combine)
       a.items = p->d_items + d.fq_base;
       a.masks = p->d_masks + d.fq_base;
+      a.pidx = p->d_pidx + (size_t)d.fq_base * PADW_H;
+      a.poff = p->d_poff + (size_t)d.fq_base * PADW_H;
       a.n_items = (int)d.fq_n;
       a.n_heavy = 0;
     }
@@ -971,11 +1019,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       if (alias && d.ba_on) {
         // children whose adjoint is not routed; absolute output rows (route
         // tops write their chain's bottom) and value rows
-        a.items = p->d_items + d.ba.i_base;
-        a.masks = p->d_masks + d.ba.i_base;
-        a.n_items = (int)d.ba.i_n;
-        a.heavy = p->d_heavy + d.ba.h_base;
-        a.n_heavy = (int)d.ba.h_n;
+        set_items(a, p, d.ba);
         a.off = p->d_aoff + d.ba.off_base;
         a.idx = p->d_aidx + d.ba.e_base;
         a.omap = p->d_omap + d.ba.map_base;

@@ -44,6 +44,12 @@ struct LayerArgs {
   const int* omap;
   const int* xmap;
   T* mbase;
+  // padded per-item index data (klay.cu pad_items; PADW ints per item):
+  // edge indices, raw segment offsets, and for alias sets omap / xmap entries
+  const int* pidx;
+  const int* poff;
+  const int* pmap;
+  const int* pxmap;
   int rev;            // visit the column chunks last to first (L2 reuse across launches)
 };
 

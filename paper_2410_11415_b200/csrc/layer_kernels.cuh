@@ -336,30 +336,42 @@ struct ItemRegs {
   int map, xmap;
 };
 
-// index loads of one item whose descriptor (it, mask) is already known
+// Index data of item k (descriptor it/mask). Items with <= PADW edges have
+// their edge indices, raw segment offsets and maps in padded per-item rows
+// (klay.cu pad_items), loaded together with the descriptor: one round trip.
+// Longer items load their indices after the descriptor.
+constexpr int PADW = 32;
+
 template <typename T>
-__device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int4 it, unsigned mask,
-                                                   int lane) {
+__device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int k, int4 it,
+                                                   unsigned mask, int lane) {
   ItemRegs r;
   r.it = it;
   r.mask = mask;
+  const size_t pk = (size_t)k * PADW + lane;
+  const int p0 = __ldg(a.pidx + pk);
+  const int o0 = __ldg(a.poff + pk);
+  r.map = a.pmap ? __ldg(a.pmap + pk) : 0;
+  r.xmap = a.pxmap ? __ldg(a.pxmap + pk) : 0;
   const int ne = r.it.w - r.it.z;
+  if (ne <= PADW) {
+    r.idx[0] = p0;
 #pragma unroll
-  for (int q = 0; q < TASK_EDGES / 32; ++q) {
-    const int e = q * 32 + lane;
-    r.idx[q] = (ne <= TASK_EDGES && e < ne) ? __ldg(a.idx + r.it.z + e) : 0;
+    for (int q = 1; q < TASK_EDGES / 32; ++q) r.idx[q] = 0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < TASK_EDGES / 32; ++q) {
+      const int e = q * 32 + lane;
+      r.idx[q] = (ne <= TASK_EDGES && e < ne) ? __ldg(a.idx + r.it.z + e) : 0;
+    }
   }
-  const int nn = r.it.y - r.it.x;
-  r.off = (r.it.y > 0 && lane <= nn) ? __ldg(a.off + r.it.x + lane) - r.it.z : 0;
-  const bool in = lane < (r.it.y > 0 ? nn : 1);
-  r.map = (a.omap && in) ? __ldg(a.omap + r.it.x + lane) : 0;
-  r.xmap = (a.xmap && in) ? __ldg(a.xmap + r.it.x + lane) : 0;
+  r.off = r.it.y > 0 ? o0 - r.it.z : 0;  // segment offsets relative to the first edge
   return r;
 }
 
 template <typename T>
 __device__ __forceinline__ ItemRegs load_item_regs(const LayerArgs<T>& a, int item, int lane) {
-  return item_regs_from(a, __ldg(a.items + item), __ldg(a.masks + item), lane);
+  return item_regs_from(a, item, __ldg(a.items + item), __ldg(a.masks + item), lane);
 }
 
 __device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r, int lane) {
@@ -880,7 +892,8 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
   }
   __syncwarp();
   ItemRegs next;
-  if (t.n > 0 && w < t.layer[0].n_items) next = item_regs_from(t.layer[0], desc[0].it, desc[0].mask, lane);
+  if (t.n > 0 && w < t.layer[0].n_items)
+    next = item_regs_from(t.layer[0], w, desc[0].it, desc[0].mask, lane);
   // all of the above is plan data: wait for the previous kernel's values
   // only now (programmatic dependent launch), and let the next kernel's
   // blocks take the SMs the tail leaves idle for their own prologue
@@ -893,7 +906,7 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
     stamp(i, 0);
     const ItemRegs cur = next;
     if (i + 1 < t.n && w < t.layer[i + 1].n_items)
-      next = item_regs_from(t.layer[i + 1], desc[i + 1].it, desc[i + 1].mask, lane);
+      next = item_regs_from(t.layer[i + 1], w, desc[i + 1].it, desc[i + 1].mask, lane);
     if (!t.debug_skip) {
       for (int it = w; it < a.n_items; it += cw) {
         __syncwarp();  // previous item done with ib
