@@ -534,9 +534,6 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
 
   // ===================== long segment / leaf =====================
   const bool leaf = it.y < 0;
-#ifdef KLAY_SKIP_LONG  // (timing experiment only: wrong results)
-  if (!leaf) return;
-#endif
   const int node = a.omap ? wmap[0] : it.x;  // output (see the short path)
   const int xnode = a.xmap ? wxmap[0] : it.x;
   const int t0 = leaf ? 0 : 1;      // first tail edge (relative)
