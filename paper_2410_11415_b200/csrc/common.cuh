@@ -268,13 +268,20 @@ struct LseOp {
         // first element: exp(x - x) = 1, or 0 for an all -inf prefix (NaN -> 0)
         m.v[c] = xv;
         t.v[c] = (xv == T(-INFINITY)) ? T(0) : T(1);
-      } else if (xv > m.v[c]) {
-        t.v[c] = t.v[c] * kexp(m.v[c] - xv) + T(1);
-        m.v[c] = xv;
-      } else if (fabs(xv) != T(INFINITY)) {
-        // (xv == +inf here means m == +inf: exp(NaN) -> 0 in the reference;
-        // a NaN xv makes the sum NaN, which result() turns into NaN)
-        t.v[c] = t.v[c] + kexp(xv - m.v[c]);
+      } else {
+        // branch-free (lanes hold different columns): one exp(-|x - m|)
+        //   x > m:  t = t * exp(m - x) + 1, m = x   (rescale to the new peak)
+        //   x <= m: t = t + exp(x - m)
+        // d is NaN for inf - inf (equal infinite peak and element: the
+        // reference masks that term to 0) or for a NaN input (kept: the sum
+        // turns NaN, which result() reports as NaN)
+        const T mv = m.v[c];
+        const T d = xv - mv;
+        T e = kexp(-fabs(d));
+        if (d != d) e = (xv != xv || mv != mv) ? d : T(0);
+        const bool up = d > T(0);
+        t.v[c] = up ? t.v[c] * e + T(1) : t.v[c] + e;
+        m.v[c] = up ? xv : mv;
       }
     }
     ++k;

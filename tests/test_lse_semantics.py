@@ -1,5 +1,6 @@
 """The online logsumexp recurrence of the CUDA kernels (csrc/common.cuh:
-LseOp::push / result and lse_merge for split segments), restated in Python,
+LseOp::push (branch-free form) / result and lse_merge for split segments),
+restated in Python,
 equals the reference's masked max-trick logsumexp (engine.py:274-282) on
 every combination of finite, +-inf and NaN elements, whole or split into
 leaves. CPU only: a design check of the recurrence the GPU tests exercise."""
@@ -18,10 +19,15 @@ def _push_all(xs):
     for k, x in enumerate(xs):
         if k == 0:
             m, t = x, (0.0 if x == -INF else 1.0)
-        elif x > m:
-            t, m = t * np.exp(m - x) + 1.0, x
-        elif abs(x) != INF:
-            t = t + np.exp(x - m)
+            continue
+        d = x - m
+        e = np.exp(-abs(d))
+        if d != d:
+            e = d if (x != x or m != m) else 0.0
+        if d > 0:
+            t, m = t * e + 1.0, x
+        else:
+            t = t + e
     return m, t
 
 
