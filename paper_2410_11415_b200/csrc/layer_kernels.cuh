@@ -209,22 +209,14 @@ struct BwdGather {
     Vec<T> r;
     if constexpr (MODE == BW_LOGSUM) {
       // g[parent] * exp(child - parent); NaN/inf weights -> 0 (engine.py:346-352).
-      // A parent equal to its child (a unary sum, epsilon 0) has weight
-      // exp(0) = 1, or 0 when both are -inf (exp(NaN) masked): no exp needed.
-      bool same = true;
+      // (Unary parents never get here: their edges are flagged, see unary().
+      // A child equal to its parent gets exp(0) = 1 exactly, so no special
+      // case: one uniform path, no lane divergence.)
 #pragma unroll
-      for (int c = 0; c < N; ++c) same &= (x.v[c] == P.v[c]);
-      if (same) {
-        // (x == P excludes NaN; +-inf children give exp(NaN) -> 0)
-#pragma unroll
-        for (int c = 0; c < N; ++c) r.v[c] = isfinite(x.v[c]) ? g.v[c] : g.v[c] * T(0);
-      } else {
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-          T w = kexp(x.v[c] - P.v[c]);
-          w = isfinite(w) ? w : T(0);
-          r.v[c] = g.v[c] * w;
-        }
+      for (int c = 0; c < N; ++c) {
+        T w = kexp(x.v[c] - P.v[c]);
+        w = isfinite(w) ? w : T(0);
+        r.v[c] = g.v[c] * w;
       }
     } else {
       // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
