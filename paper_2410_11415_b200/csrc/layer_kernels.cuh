@@ -574,11 +574,14 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
     };
     if constexpr (RK == RK_SUM) {
       if (8 * t < mainend) {
-        // a full round of numpy's 8 pairwise accumulators
+        // a full round of numpy's 8 pairwise accumulators (t is warp-uniform:
+        // two loops instead of a per-element select)
+        if (t == 0) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const Vec<T> xv = val(k);
-          r[k] = (t == 0) ? xv : vadd(r[k], xv);
+          for (int k = 0; k < 8; ++k) r[k] = val(k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) r[k] = vadd(r[k], val(k));
         }
       } else {
         if (m >= 8) res = combine8(r);
