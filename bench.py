@@ -468,7 +468,7 @@ def run_gpu_arm(args):
     launches_per_step = None
 
     # the timed step replays one CUDA graph holding the whole fwd + bwd
-    # (117 kernels for config C); the instrumented step below launches them
+    # (~100 kernels for config C); the instrumented step below launches them
     # one by one on the stream to time each
     cap = plan.capture(B, dt, _lib.KLAY_LOG, backward=True)
     cap.weights.copy_(w_dev)
@@ -517,16 +517,16 @@ def run_gpu_arm(args):
     plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
     plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
     import ctypes
-    cap = 4 * len(tc.layers) + 16
-    kinds = (ctypes.c_int32 * cap)()
-    layers = (ctypes.c_int32 * cap)()
-    tms = (ctypes.c_float * cap)()
+    nslots = 4 * len(tc.layers) + 16
+    kinds = (ctypes.c_int32 * nslots)()
+    layers = (ctypes.c_int32 * nslots)()
+    tms = (ctypes.c_float * nslots)()
     nrec = ctypes.c_int32()
-    lib.klay_profiler_end(cap, kinds, layers, tms, ctypes.byref(nrec))
+    lib.klay_profiler_end(nslots, kinds, layers, tms, ctypes.byref(nrec))
     fwd_b, bwd_b = layer_bytes(tc, s, B)
     per_kind = {0: [0.0, 0.0, 0], 1: [0.0, 0.0, 0]}
     other_ms = 0.0
-    for i in range(min(nrec.value, cap)):
+    for i in range(min(nrec.value, nslots)):
         k, l, t = kinds[i], layers[i], tms[i]
         if k in (0, 1):
             per_kind[k][0] += t
