@@ -423,7 +423,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       pairs.push_back(make_int2((int)(p->layer_row[nl] + i) | (tf[nl][i] ? INT32_MIN : 0), srow[nl][i]));
     }
   // routes
-  static const int dbg_routes = [] {  // KLAY_ROUTES=0: none, 1: unmasked only (debug)
+  static const int dbg_routes = [] {  // KLAY_ROUTES=0: no routes, 1: unmasked only (A/B, debug)
     const char* e = getenv("KLAY_ROUTES");
     return (e && *e) ? atoi(e) : 2;
   }();
@@ -443,7 +443,6 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       }
       // a masked route needs a computed bottom to write the mask
       if (masked && (ali[nl][i] || nl == 0 || dbg_routes < 2)) continue;
-      if (dbg_routes >= 10 && tl - nl > dbg_routes - 10) continue;  // (debug: span limit)
       for (int sl = nl, sj = (int)i; sl < tl; sj = up[sl][sj], ++sl) skip[sl][sj] = 1;
       redirect[tl][t] = (int)(p->layer_row[nl] + i) | (masked ? INT32_MIN : 0);
       if (masked) mrow[nl][i] = (int)(p->layer_row[tl] + t);
