@@ -598,8 +598,8 @@ def run_gpu_arm(args):
         e2e = {"value": world * B * n_e2e / el, "unit": "evals/s",
                "h2d_bytes_per_step": int(w_host.size * 4),
                "d2h_bytes_per_step": int(out.nbytes + g.nbytes),
-               "api": "engine.gradient(log_domain=True, dtype=float32): numpy in/out, pinned "
-                      "H2D + graph replay + D2H per step"}
+               "api": "engine.gradient(log_domain=True, dtype=float32): numpy in/out; one "
+                      "CUDA graph per call holding the pinned H2D copy, fwd, bwd and D2H copies"}
 
     extra = None
     if world == 1 and not args.no_extra:

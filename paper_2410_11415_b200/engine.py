@@ -319,9 +319,10 @@ class DevicePlan:
         return values
 
     def capture(self, batch: int, dtype, semiring: int, epsilon: float = 0.0,
-                backward: bool = True, seeded: bool = False) -> "CapturedPass":
+                backward: bool = True, seeded: bool = False,
+                host_io: bool = False) -> "CapturedPass":
         """A CUDA-graph-captured forward (+ backward) over fixed buffers."""
-        return CapturedPass(self, batch, dtype, semiring, epsilon, backward, seeded)
+        return CapturedPass(self, batch, dtype, semiring, epsilon, backward, seeded, host_io)
 
     def workspace(self, batch: int, dtype):
         torch = _torch()
@@ -372,7 +373,7 @@ class CapturedPass:
     """
 
     def __init__(self, plan: DevicePlan, batch: int, dtype, semiring: int, epsilon: float = 0.0,
-                 backward: bool = True, seeded: bool = False):
+                 backward: bool = True, seeded: bool = False, host_io: bool = False):
         torch = _torch()
         dt = _resolve_dtype(dtype)
         tdt = torch.float64 if dt == np.float64 else torch.float32
@@ -387,13 +388,30 @@ class CapturedPass:
         self.values = plan.alloc_values(batch, dt, retain=backward)
         self._fw = plan.forward_workspace(batch, dt)
         self._bw = plan.workspace(batch, dt) if backward else None
+        # host_io: pinned host buffers h_weights / h_seed / h_out / h_grad, the
+        # copies captured in the graph too (one launch per call)
+        self.host_io = host_io
+        if host_io:
+            pin = dict(dtype=tdt, pin_memory=True)
+            self.h_weights = torch.empty(self.weights.shape, **pin)
+            self.h_out = torch.empty(self.outputs.shape, **pin)
+            self.h_grad = torch.empty(self.grads.shape, **pin) if backward else None
+            self.h_seed = torch.empty(self.seed.shape, **pin) if seeded else None
 
         def run():
+            if host_io:
+                self.weights.copy_(self.h_weights, non_blocking=True)
+                if seeded:
+                    self.seed.copy_(self.h_seed, non_blocking=True)
             plan.forward(self.weights, semiring, dt, retain=backward, epsilon=epsilon,
                          values=self.values, outputs=self.outputs, workspace=self._fw)
             if backward:
                 plan.backward(self.values, batch, semiring, dt, seed=self.seed, grads=self.grads,
                               workspace=self._bw)
+            if host_io:
+                self.h_out.copy_(self.outputs, non_blocking=True)
+                if backward:
+                    self.h_grad.copy_(self.grads, non_blocking=True)
 
         # warm up outside capture (kernel attributes, lazy module loading)
         side = torch.cuda.Stream(device=dev)
@@ -613,24 +631,17 @@ def gradient(tc, weights: WeightAssignment, log_domain: bool = False, epsilon: f
     key = (id(plan), B, np.dtype(dt).str, code, float(epsilon), seed is not None)
     cap = _PASS_CACHE.get(key)
     if cap is None or cap.plan is not plan:
-        cap = plan.capture(B, dt, code, epsilon=epsilon, backward=True, seeded=seed is not None)
-        tdt = cap.weights.dtype
-        cap.h_weights = torch.empty(cap.weights.shape, dtype=tdt, pin_memory=True)
-        cap.h_out = torch.empty(cap.outputs.shape, dtype=tdt, pin_memory=True)
-        cap.h_grad = torch.empty(cap.grads.shape, dtype=tdt, pin_memory=True)
-        if seed is not None:
-            cap.h_seed = torch.empty(cap.seed.shape, dtype=tdt, pin_memory=True)
+        cap = plan.capture(B, dt, code, epsilon=epsilon, backward=True, seeded=seed is not None,
+                           host_io=True)
         _PASS_CACHE[key] = cap
-    cap.h_weights.numpy()[...] = w.values
-    cap.weights.copy_(cap.h_weights, non_blocking=True)
     if seed is not None:
         sd = np.asarray(seed, dtype=np.dtype(dt))
         if sd.shape != (B, tc.num_roots):
             raise EvalError(f"seed must have shape {(B, tc.num_roots)}")
+    stream = torch.cuda.current_stream(plan.device)
+    cap.h_weights.numpy()[...] = w.values  # (idle: the previous call synchronized)
+    if seed is not None:
         cap.h_seed.numpy()[...] = sd
-        cap.seed.copy_(cap.h_seed, non_blocking=True)
-    cap.replay()
-    cap.h_out.copy_(cap.outputs, non_blocking=True)
-    cap.h_grad.copy_(cap.grads, non_blocking=True)
-    torch.cuda.current_stream(plan.device).synchronize()
+    cap.replay()  # H2D, forward, backward, D2H: one graph launch
+    stream.synchronize()
     return cap.h_out.numpy().copy(), cap.h_grad.numpy().copy()
