@@ -220,12 +220,14 @@ struct BwdGather {
       }
     } else {
       // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
-      // child gets g * (product of nonzero siblings) iff it is the only zero
+      // child gets g * (product of nonzero siblings) iff it is the only zero,
+      // any child of a segment holding a zero gets exactly 0 (a zero product
+      // sends the rare segments with a zero, or an underflow, to zero_path)
       bool any_zero = false;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         r.v[c] = (g.v[c] * P.v[c]) / x.v[c];
-        any_zero |= (x.v[c] == T(0));
+        any_zero |= (x.v[c] == T(0)) | (P.v[c] == T(0));
       }
       if (any_zero) zero_path(r, g, row, x);
     }
@@ -247,8 +249,10 @@ struct BwdGather {
       }
     }
 #pragma unroll
-    for (int c = 0; c < N; ++c)
+    for (int c = 0; c < N; ++c) {
       if (x.v[c] == T(0)) r.v[c] = (zc[c] == 1) ? g.v[c] * pnz[c] : T(0);
+      else if (zc[c] > 0) r.v[c] = T(0);  // (a zero sibling: 0 even for an infinite adjoint)
+    }
   }
 };
 

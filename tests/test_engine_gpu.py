@@ -457,6 +457,7 @@ def test_alias_and_tail_extremes(cuda, tail_edges):
     r = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
          os.path.join(os.path.dirname(__file__), "test_engine_gpu.py"),
-         "-k", "golden_small or nonfinite or backward_only or consumer"],
+         os.path.join(os.path.dirname(__file__), "test_fuzz_gpu.py"),
+         "-k", "golden_small or nonfinite or backward_only or consumer or random_circuits"],
         env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
