@@ -221,13 +221,15 @@ struct BwdGather {
     } else {
       // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
       // child gets g * (product of nonzero siblings) iff it is the only zero,
-      // any child of a segment holding a zero gets exactly 0 (a zero product
-      // sends the rare segments with a zero, or an underflow, to zero_path)
+      // any child of a segment holding a zero gets exactly 0. A segment with
+      // a zero has a product of 0, or NaN (0 * inf): both send it to
+      // zero_path, which counts the zeros (an underflow or a NaN input with
+      // no zero keeps the plain formula, as in the reference)
       bool any_zero = false;
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         r.v[c] = (g.v[c] * P.v[c]) / x.v[c];
-        any_zero |= (x.v[c] == T(0)) | (P.v[c] == T(0));
+        any_zero |= (x.v[c] == T(0)) | (P.v[c] == T(0)) | (P.v[c] != P.v[c]);
       }
       if (any_zero) zero_path(r, g, row, x);
     }

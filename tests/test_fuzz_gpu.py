@@ -12,14 +12,14 @@ from conftest import rel_close
 pytestmark = pytest.mark.gpu
 
 
-def random_circuit(seed, K=24, L=9, wmax=60):
+def random_circuit(seed, K=24, L=9, wmax=60, grow=1):
     from paper_2410_11415_b200.tensorized import Literal, TensorizedCircuit, TensorLayer, validate
     rng = np.random.default_rng(seed)
     layers = []
     prev = K
     for l in range(L):
         op = "prod" if l % 2 == 0 else "sum"
-        W = int(rng.integers(max(1, prev // 3), max(2, min(wmax, prev + 8))))
+        W = int(rng.integers(max(1, prev // 3), max(2, min(wmax, grow * prev + 8))))
         W = max(1, min(W, prev)) if l == L - 1 else W
         # every previous node feeds some parent; extra edges give fan-in > 1
         owner = rng.integers(0, W, size=prev)
@@ -53,7 +53,7 @@ def test_random_circuits_match_oracle(cuda, seed):
     tc = random_circuit(seed)
     plan = device_plan(tc)
     rng = np.random.default_rng(100 + seed)
-    B = 37
+    B = (37, 1, 64, 5)[seed % 4]
     w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
     w[rng.uniform(size=w.shape) < 0.04] = 0.0
     # real fp64: bit-exact values and gradients
@@ -78,3 +78,48 @@ def test_random_circuits_match_oracle(cuda, seed):
     nv = _NodeValues(plan, vals, B)
     for l in range(len(tr)):
         rel_close(nv[l], tr[l], 1e-12, 1e-12)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_wide_circuits_all_semirings(cuda, seed):
+    """Wider random circuits (regular layer kernels, aliases and routes at the
+    default tail): fp32 real bit-exact vs the reference's own fp32 run, fp32 log
+    within rel 1e-5 of fp64, Boolean (bit-packed) and max-product bit-exact,
+    seeded backward."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan, engine
+    tc = random_circuit(1000 + seed, K=40, L=11, wmax=700, grow=3)
+    plan = device_plan(tc)
+    rng = np.random.default_rng(7 + seed)
+    B = (1, 45, 130, 33)[seed % 4]
+    w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
+    w[rng.uniform(size=w.shape) < 0.03] = 0.0
+    # fp32 real, seeded backward: bit-exact vs the oracle in fp32
+    w32 = w.astype(np.float32)
+    seed_m = rng.uniform(-1, 1, size=(B, tc.num_roots)).astype(np.float32)
+    x = torch.tensor(w32, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_REAL, np.float32)
+    g = plan.backward(vals, B, _lib.KLAY_REAL, np.float32, seed=torch.tensor(seed_m, device=cuda))
+    ref, tr = oracle.forward(tc, w32, "real")
+    assert np.array_equal(out.cpu().numpy(), ref, equal_nan=True)
+    np.testing.assert_array_equal(g.cpu().numpy(), oracle.backward(tc, tr, "real", seed_m))
+    # fp32 log vs the fp64 oracle
+    with np.errstate(divide="ignore"):
+        lw = np.log(w)
+    x = torch.tensor(lw.astype(np.float32), device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_LOG, np.float32)
+    g = plan.backward(vals, B, _lib.KLAY_LOG, np.float32)
+    with np.errstate(all="ignore"):
+        ref, tr = oracle.forward(tc, lw, "log")
+        gref = oracle.backward(tc, tr, "log")
+    rel_close(out.cpu().numpy(), ref, 1e-5, 1e-5)
+    rel_close(g.cpu().numpy(), gref, 1e-5, 1e-5)
+    # Boolean on 0/1 inputs (bit-packed path) and max-product: bit-exact
+    wb = (rng.uniform(size=w.shape) < 0.6).astype(np.float64)
+    ref, _ = oracle.forward(tc, wb, "bool", retain=False)
+    got = engine.evaluate_semiring(tc, engine.WeightAssignment(wb), "bool")
+    assert np.array_equal(got, ref)
+    ref, _ = oracle.forward(tc, w, "maxprod", retain=False)
+    got = engine.evaluate_semiring(tc, engine.WeightAssignment(w), "maxprod")
+    assert np.array_equal(got, ref)
