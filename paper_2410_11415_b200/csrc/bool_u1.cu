@@ -17,6 +17,10 @@ int launch_forward_tail_u1(const TailArgs<unsigned>& t, int cluster, cudaStream_
   return launch_tail<unsigned, RK_AND, RK_OR, G, G>(t, cluster, s);
 }
 
+int launch_forward_micro_u1(const MicroArgs<unsigned>& m, cudaStream_t s) {
+  return launch_micro<unsigned, RK_AND, RK_OR>(m, s);
+}
+
 // one thread per (input slot, 32-row word): bit j of word w = row 32w + j
 template <typename TI>
 __global__ void pack_inputs_kernel(const TI* __restrict__ w, unsigned* __restrict__ n0, int K,

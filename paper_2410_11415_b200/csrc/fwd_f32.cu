@@ -33,4 +33,13 @@ int launch_forward_tail(int sr, const TailArgs<float>& t, int cluster, cudaStrea
   }
 }
 
+int launch_forward_micro(int sr, const MicroArgs<float>& m, cudaStream_t s) {
+  switch (sr) {
+    case SR_REAL: return launch_micro<float, RK_PROD, RK_SUM>(m, s);
+    case SR_LOG: return launch_micro<float, RK_SUM, RK_LSE>(m, s);
+    case SR_BOOL: return launch_micro<float, RK_MIN, RK_MAX>(m, s);
+    default: return launch_micro<float, RK_PROD, RK_MAX>(m, s);
+  }
+}
+
 }  // namespace klay

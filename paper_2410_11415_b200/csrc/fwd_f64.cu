@@ -33,4 +33,13 @@ int launch_forward_tail(int sr, const TailArgs<double>& t, int cluster, cudaStre
   }
 }
 
+int launch_forward_micro(int sr, const MicroArgs<double>& m, cudaStream_t s) {
+  switch (sr) {
+    case SR_REAL: return launch_micro<double, RK_PROD, RK_SUM>(m, s);
+    case SR_LOG: return launch_micro<double, RK_SUM, RK_LSE>(m, s);
+    case SR_BOOL: return launch_micro<double, RK_MIN, RK_MAX>(m, s);
+    default: return launch_micro<double, RK_PROD, RK_MAX>(m, s);
+  }
+}
+
 }  // namespace klay

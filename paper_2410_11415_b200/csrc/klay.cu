@@ -98,6 +98,12 @@ const int g_chunk_order = [] {
 int chunk_rev(int l) { return g_chunk_order == 1 ? (l & 1) : g_chunk_order == 2 ? ((l >> 1) & 1) : 0; }
 
 // KLAY_NO_ALIAS=1: every sum row is computed and read (A/B switch)
+// KLAY_NO_MICRO=1: the thinnest layers run in the persistent tail too (A/B switch)
+const bool g_no_micro = [] {
+  const char* e = getenv("KLAY_NO_MICRO");
+  return e && *e && *e != '0';
+}();
+
 const bool g_no_alias = [] {
   const char* e = getenv("KLAY_NO_ALIAS");
   return e && *e && *e != '0';
@@ -322,6 +328,10 @@ struct KlayPlan {
   int64_t n_alias = 0;
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
   int32_t tail_from = 0;  // first layer of the persistent tail (L = no tail)
+  int32_t micro_from = 0;  // first layer of the forward micro tail (>= tail_from; L = none)
+  std::vector<int> micro_at;  // per micro layer: offset of its CSR in d_micro
+  int* d_micro = nullptr;     // packed micro-tail CSR ([W+1] local offsets, [E] indices per layer)
+  int micro_ints = 0;
 };
 
 extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
@@ -349,6 +359,7 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_poff);
   cudaFree(p->d_pmap);
   cudaFree(p->d_pmap2);
+  cudaFree(p->d_micro);
   delete p;
 }
 
@@ -708,6 +719,32 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   }
   p->total_rows = row;
   p->WL = prev_w;
+  // forward micro tail: the longest suffix of tail layers that fit it
+  // (widths and fan-ins bounded, CSR inside MICRO_CSR ints)
+  std::vector<int> micro;
+  {
+    int32_t mf = num_layers;
+    int64_t ints = 0;
+    while (mf > tail_from && num_layers - mf < MICRO_MAX_LAYERS) {
+      const LayerDesc& d = p->layers[mf - 1];
+      int maxfan = 0;
+      for (int64_t i = 0; i < d.W; ++i)
+        maxfan = std::max(maxfan, off[d.off_base + i + 1] - off[d.off_base + i]);
+      if (d.W > MICRO_W || d.Wprev > MICRO_W || maxfan > MICRO_FAN ||
+          ints + d.W + 1 + d.E > MICRO_CSR)
+        break;
+      ints += d.W + 1 + d.E;
+      --mf;
+    }
+    p->micro_from = mf;
+    for (int32_t l = mf; l < num_layers; ++l) {
+      const LayerDesc& d = p->layers[l];
+      p->micro_at.push_back((int)micro.size());
+      for (int64_t i = 0; i <= d.W; ++i) micro.push_back(off[d.off_base + i]);
+      for (int64_t e = 0; e < d.E; ++e) micro.push_back(src[d.e_base + e]);
+    }
+    p->micro_ints = (int)micro.size();
+  }
   if (num_layers >= 2 && row < (1LL << 30)) {
     build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
                   alias_rows,
@@ -744,7 +781,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       (rc = upload(&p->d_aoff, aoff)) || (rc = upload(&p->d_aidx, aidx)) ||
       (rc = upload(&p->d_omap, omap)) || (rc = upload(&p->d_alias, alias_rows)) ||
       (rc = upload(&p->d_pidx, pidx)) || (rc = upload(&p->d_poff, poff)) ||
-      (rc = upload(&p->d_pmap, pmap)) || (rc = upload(&p->d_pmap2, pxmap))) {
+      (rc = upload(&p->d_pmap, pmap)) || (rc = upload(&p->d_pmap2, pxmap)) ||
+      (rc = upload(&p->d_micro, micro))) {
     plan_free(p);
     return rc;
   }
@@ -853,8 +891,9 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     KLAY_CUDA(cudaMemsetAsync(hcount, 0, counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld), s));
   }
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
+  const int32_t micro_from = (g_no_tail || g_no_micro) ? p->L : p->micro_from;
   TailArgs<T>* tail = nullptr;
-  if (tail_from < p->L) {
+  if (tail_from < micro_from) {
     tail = new TailArgs<T>();
     tail->n = 0;
     tail->debug_skip = g_tail_debug ? 1 : 0;
@@ -863,6 +902,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   // unary-sum aliases need the rows two layers down: backward-only traces
   constexpr bool U1_ = std::is_same<T, unsigned>::value;
   const bool alias = !U1_ && sr == SR_LOG_ && eps == 0.0 && retain_mode == 2 && !g_no_alias;
+  MicroArgs<T> micro{};
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
@@ -892,7 +932,18 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     a.rev = chunk_rev(l);
     a.scratch = work;
     a.tpart = (long long)p->max_fslots * ld;
-    if (l >= tail_from) {
+    if (l >= micro_from) {
+      const int i = micro.n++;
+      if (i == 0) {
+        micro.in = prev;
+        micro.w_in = (int)d.Wprev;
+      }
+      // ping-pong mode: only the last layer's rows are read afterwards
+      micro.out[i] = (retain || l == p->L - 1) ? cur : nullptr;
+      micro.w[i] = (int)d.W;
+      micro.csr_at[i] = p->micro_at[l - p->micro_from];
+      micro.prod[i] = d.prod ? 1 : 0;
+    } else if (l >= tail_from) {
       tail->layer[tail->n++] = a;
     } else {
       a.hcount = hcount;
@@ -904,7 +955,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   }
   if (tail) {
     const LayerDesc& d0 = p->layers[tail_from];
-    const LayerDesc& dl = p->layers[p->L - 1];
+    const LayerDesc& dl = p->layers[micro_from - 1];
     tail->pf_ptr[0] = p->d_src + d0.e_base;
     tail->pf_bytes[0] = (dl.e_base + dl.E - d0.e_base) * (long long)sizeof(int);
     tail->pf_ptr[1] = p->d_off + d0.off_base;
@@ -927,7 +978,21 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
                                             cudaGetErrorString(cudaGetLastError()));
     g_launches += n;
-    if (g_tail_trace) tail_trace_dump("forward", p->L - tail_from);
+    if (g_tail_trace) tail_trace_dump("forward", micro_from - tail_from);
+  }
+  if (micro.n > 0) {
+    micro.csr = p->d_micro;
+    micro.csr_ints = p->micro_ints;
+    micro.V = V;
+    micro.ld = ld;
+    micro.eps = (T)eps;
+    LaunchScope ls(s, 6, micro_from + 1);
+    int n;
+    if constexpr (U1) n = launch_forward_micro_u1(micro, s);
+    else n = launch_forward_micro(sr, micro, s);
+    if (n == 0) return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
+                                            cudaGetErrorString(cudaGetLastError()));
+    g_launches += n;
   }
   if (outputs && p->R > 0) {
     LaunchScope ls(s, 2, p->L + 1);

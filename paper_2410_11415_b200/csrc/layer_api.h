@@ -68,6 +68,31 @@ struct TailArgs {
   unsigned long long* trace_ts;  // KLAY_TAIL_TRACE=1: per-layer globaltimer stamps (debug)
 };
 
+// The forward micro tail: the thinnest top layers (every width <= MICRO_W,
+// fan-in <= MICRO_FAN) evaluated by one CTA per column chunk with the layer
+// values held in shared memory; CSR offsets (local, from 0) and indices of
+// every micro layer are packed into one int block staged in shared memory.
+constexpr int MICRO_MAX_LAYERS = 64;
+constexpr int MICRO_W = 192;
+constexpr int MICRO_FAN = 8;
+constexpr int MICRO_CSR = 4096;  // ints
+template <typename T>
+struct MicroArgs {
+  const T* in;                    // rows of the layer below the first micro layer
+  T* out[MICRO_MAX_LAYERS];       // output rows per layer (null: not stored)
+  int w[MICRO_MAX_LAYERS];        // widths
+  int csr_at[MICRO_MAX_LAYERS];   // offset of the layer's [W+1 offsets, E indices] in csr
+  int prod[MICRO_MAX_LAYERS];
+  const int* csr;
+  int csr_ints;
+  int n, w_in, V;
+  long long ld;
+  T eps;
+};
+int launch_forward_micro(int sr, const MicroArgs<float>& m, cudaStream_t s);
+int launch_forward_micro(int sr, const MicroArgs<double>& m, cudaStream_t s);
+int launch_forward_micro_u1(const MicroArgs<unsigned>& m, cudaStream_t s);
+
 // forward layer: semiring x layer op -> reduction kind (RK_*)
 int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<float>& a, cudaStream_t s);
 int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<double>& a, cudaStream_t s);

@@ -960,4 +960,115 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, t) == cudaSuccess ? 1 : 0;
 }
 
+// ---- micro tail: the thinnest layers with their values in shared memory ----
+//
+// Above the persistent tail's layers the circuit narrows to a few dozen
+// nodes; there a layer is latency, not bandwidth: a cluster barrier plus an
+// L2 round trip per layer. One CTA per 512-byte column chunk holds two
+// layers' rows of its chunk in shared memory (ping-pong), reduces each node
+// from shared memory, stores the result to both shared memory and the trace,
+// and meets the other warps of the CTA at a __syncthreads per layer. The CSR
+// of all micro layers is staged once, before the PDL wait.
+
+constexpr int MICRO_WARPS = 16;
+constexpr size_t MICRO_ROWS_BYTES = (size_t)2 * MICRO_W * NV * 32 * 16;
+constexpr size_t MICRO_SMEM = MICRO_ROWS_BYTES + (size_t)MICRO_CSR * sizeof(int);
+
+template <typename T>
+__device__ __forceinline__ void sts_vec(uint4* slot, const Vec<T>& r, int lane) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    uint4 u;
+    memcpy(&u, &r.v[q * PIECE<T>], 16);
+    slot[q * 32 + lane] = u;
+  }
+}
+
+// one node over rows in shared memory, in the reference's order (n <= MICRO_FAN:
+// numpy's pairwise sum is x0 + sequential sum of the rest)
+template <typename T, int RK>
+__device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, const int* idx, int n, int lane,
+                                               T eps) {
+  auto v = [&](int e) { return lds_vec<T>(rows + (size_t)idx[e] * 32 * NV, lane); };
+  Vec<T> out = v(0);
+  if constexpr (RK == RK_SUM) {
+    if (n > 1) {
+      Vec<T> acc = v(1);
+      for (int j = 2; j < n; ++j) acc = vadd(acc, v(j));
+      out = vadd(out, acc);
+    }
+  } else if constexpr (RK == RK_LSE) {
+    if (n > 1 || eps != T(0)) {
+      LseOp<T> op;
+      op.eps = eps;
+      op.begin(n);
+      op.push(out);
+      for (int j = 1; j < n; ++j) op.push(v(j));
+      out = op.result();
+    } else {
+      out = lse_unary(out);
+    }
+  } else {
+    for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, v(j));
+  }
+  return out;
+}
+
+template <typename T, int RKP, int RKS>
+__global__ void __launch_bounds__(MICRO_WARPS * 32, 1)
+    micro_kernel(const __grid_constant__ MicroArgs<T> m) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint4* rows = reinterpret_cast<uint4*>(smem);
+  int* csr = reinterpret_cast<int*>(smem + MICRO_ROWS_BYTES);
+  constexpr size_t RV = (size_t)MICRO_W * NV * 32;  // pieces per row buffer
+  const int chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < m.csr_ints; i += blockDim.x) csr[i] = __ldg(m.csr + i);
+  const LaneCols lc = lane_cols<T>(m.V, chunk, lane);
+  const long long ld = m.ld;
+#ifndef KLAY_NO_GDC
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+  for (int r = warp; r < m.w_in; r += MICRO_WARPS)
+    sts_vec(rows + (size_t)r * NV * 32, ldv(m.in + (size_t)r * ld + lc.col, lc.nl), lane);
+  __syncthreads();
+  for (int i = 0; i < m.n; ++i) {
+    const uint4* src = rows + (i & 1) * RV;
+    uint4* dst = rows + ((i + 1) & 1) * RV;
+    const int* off = csr + m.csr_at[i];
+    const int* idx = off + m.w[i] + 1;
+    T* out = m.out[i];
+    const bool prod = m.prod[i] != 0;
+    for (int nd = warp; nd < m.w[i]; nd += MICRO_WARPS) {
+      const int e0 = off[nd], n = off[nd + 1] - e0;
+      const Vec<T> r = prod ? micro_reduce<T, RKP>(src, idx + e0, n, lane, m.eps)
+                            : micro_reduce<T, RKS>(src, idx + e0, n, lane, m.eps);
+      sts_vec(dst + (size_t)nd * NV * 32, r, lane);
+      if (out) stv(out + (size_t)nd * ld + lc.col, r, lc.na);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T, int RKP, int RKS>
+inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
+  auto kern = micro_kernel<T, RKP, RKS>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MICRO_SMEM);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((m.V + 32 * NV - 1) / (32 * NV)), 1, 1);
+  cfg.blockDim = dim3(MICRO_WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = MICRO_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, m) == cudaSuccess ? 1 : 0;
+}
+
 }  // namespace klay

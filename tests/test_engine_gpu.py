@@ -444,16 +444,18 @@ def test_backward_only_trace_matches_full_trace(cuda, name):
         assert torch.equal(a.nan_to_num(), b.nan_to_num())
 
 
-@pytest.mark.parametrize("tail_edges", ["0", "100000"])
-def test_alias_and_tail_extremes(cuda, tail_edges):
-    """The persistent tail normally takes every small circuit whole (no
-    aliases there). Re-run the golden, non-finite and trace-equality suites
-    with no tail (every unary node below the last layer aliased, routes
-    everywhere) and with an all-tail schedule (KLAY_TAIL_EDGES is read when
-    libklay loads, hence the subprocess)."""
+@pytest.mark.parametrize("tail_edges,no_micro", [("0", "0"), ("100000", "0"), ("256", "1")])
+def test_alias_and_tail_extremes(cuda, tail_edges, no_micro):
+    """The persistent tail (and its shared-memory micro tail) normally takes
+    every small circuit whole (no aliases there). Re-run the golden,
+    non-finite and trace-equality suites with no tail (every unary node below
+    the last layer aliased, routes everywhere), with an all-tail schedule, and
+    with the micro tail off (the thinnest layers in the cluster tail);
+    KLAY_TAIL_EDGES / KLAY_NO_MICRO are read when libklay loads, hence the
+    subprocess."""
     import subprocess
     import sys
-    env = dict(os.environ, KLAY_TAIL_EDGES=tail_edges)
+    env = dict(os.environ, KLAY_TAIL_EDGES=tail_edges, KLAY_NO_MICRO=no_micro)
     r = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
          os.path.join(os.path.dirname(__file__), "test_engine_gpu.py"),
