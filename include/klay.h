@@ -216,7 +216,7 @@ KLAY_API int64_t klay_launch_count(void);
  * 0 = forward layer kernel, 1 = backward layer kernel, 2 = forward
  * boundary (inputs / outputs), 3 = backward boundary (seeds / grads),
  * 4 / 5 = forward / backward persistent tail (layers >= `layers`),
- * 6 = forward micro tail (the thinnest layers, all >= `layers`);
+ * 6 / 7 = forward / backward micro tail (the thinnest layers, all >= `layers`);
  * `layers` holds the 1-based gate layer (0 / L+1 for boundary kernels). */
 KLAY_API int klay_profiler_begin(void);
 KLAY_API int klay_profiler_end(int32_t max_records, int32_t* kinds, int32_t* layers, float* ms,

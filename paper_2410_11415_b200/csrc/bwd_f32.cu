@@ -20,4 +20,8 @@ int launch_backward_tail(int domain, const TailArgs<float>& t, int cluster, cuda
   return launch_tail<float, RK_SUM, RK_SUM, BwdGather<float, BW_REALPROD>, PASS>(t, cluster, s);
 }
 
+int launch_backward_micro(const MicroBwdArgs<float>& m, cudaStream_t s) {
+  return launch_micro_bwd<float>(m, s);
+}
+
 }  // namespace klay

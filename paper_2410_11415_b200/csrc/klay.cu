@@ -332,6 +332,10 @@ struct KlayPlan {
   std::vector<int> micro_at;  // per micro layer: offset of its CSR in d_micro
   int* d_micro = nullptr;     // packed micro-tail CSR ([W+1] local offsets, [E] indices per layer)
   int micro_ints = 0;
+  int32_t microb_from = 0;  // first layer of the backward micro tail (>= tail_from; L = none)
+  std::vector<int> microb_at;  // per layer from microb_from: offset of its transposed CSR
+  int* d_microb = nullptr;
+  int microb_ints = 0;
 };
 
 extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
@@ -360,6 +364,7 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_pmap);
   cudaFree(p->d_pmap2);
   cudaFree(p->d_micro);
+  cudaFree(p->d_microb);
   delete p;
 }
 
@@ -745,6 +750,31 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     }
     p->micro_ints = (int)micro.size();
   }
+  // backward micro tail: the same over the transposed CSR (fan-out bounded)
+  std::vector<int> microb;
+  {
+    int32_t mf = num_layers;
+    int64_t ints = 0;
+    while (mf > tail_from && num_layers - mf < MICRO_MAX_LAYERS) {
+      const LayerDesc& d = p->layers[mf - 1];
+      int maxfan = 0;
+      for (int64_t j = 0; j < d.Wprev; ++j)
+        maxfan = std::max(maxfan, toff[d.toff_base + j + 1] - toff[d.toff_base + j]);
+      if (d.W > MICRO_W || d.Wprev > MICRO_W || maxfan > MICRO_FAN ||
+          ints + d.Wprev + 1 + d.E > MICRO_CSR)
+        break;
+      ints += d.Wprev + 1 + d.E;
+      --mf;
+    }
+    p->microb_from = mf;
+    for (int32_t l = mf; l < num_layers; ++l) {
+      const LayerDesc& d = p->layers[l];
+      p->microb_at.push_back((int)microb.size());
+      for (int64_t j = 0; j <= d.Wprev; ++j) microb.push_back(toff[d.toff_base + j]);
+      for (int64_t e = 0; e < d.E; ++e) microb.push_back(tpar[d.e_base + e]);
+    }
+    p->microb_ints = (int)microb.size();
+  }
   if (num_layers >= 2 && row < (1LL << 30)) {
     build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
                   alias_rows,
@@ -782,7 +812,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       (rc = upload(&p->d_omap, omap)) || (rc = upload(&p->d_alias, alias_rows)) ||
       (rc = upload(&p->d_pidx, pidx)) || (rc = upload(&p->d_poff, poff)) ||
       (rc = upload(&p->d_pmap, pmap)) || (rc = upload(&p->d_pmap2, pxmap)) ||
-      (rc = upload(&p->d_micro, micro))) {
+      (rc = upload(&p->d_micro, micro)) || (rc = upload(&p->d_microb, microb))) {
     plan_free(p);
     return rc;
   }
@@ -1032,8 +1062,12 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   // alias outputs need the finiteness masks of a backward-only trace
   const bool alias = domain == SR_LOG_ && epsilon == 0.0 && retain_mode == 2 && !g_no_alias;
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
+  // the backward micro tail covers the log semiring (pass / log-sum layers)
+  const int32_t microb_from =
+      (g_no_tail || g_no_micro || domain != SR_LOG_) ? p->L : p->microb_from;
+  MicroBwdArgs<T> mb{};
   TailArgs<T>* tail = nullptr;
-  if (tail_from < p->L) {
+  if (tail_from < microb_from) {
     tail = new TailArgs<T>();
     tail->n = 0;
     tail->debug_skip = g_tail_debug ? 1 : 0;
@@ -1050,11 +1084,37 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.unary_ok = (domain == SR_LOG_ && epsilon == 0.0) ? 1 : 0;
     a.rev = chunk_rev(l + 1);
     a.hcount = (l >= tail_from) ? nullptr : hcount;
-    if (l >= tail_from) {
+    if (l >= microb_from) {
+      const int i = mb.n++;
+      if (i == 0) {
+        mb.gin = a.gcur;
+        mb.w_top = (int)d.W;
+      }
+      // only the lowest micro layer's adjoints are read afterwards
+      mb.gout[i] = (l == microb_from) ? a.out : nullptr;
+      mb.vpar[i] = a.ncur;
+      mb.vchild[i] = a.nprev;
+      mb.wp[i] = (int)d.W;
+      mb.wc[i] = (int)d.Wprev;
+      mb.csr_at[i] = p->microb_at[l - p->microb_from];
+      mb.logsum[i] = d.prod ? 0 : 1;
+      if (l == microb_from) {
+        mb.csr = p->d_microb;
+        mb.csr_ints = p->microb_ints;
+        mb.V = V;
+        mb.ld = ld;
+        mb.unary_ok = a.unary_ok;
+        LaunchScope ls(s, 7, microb_from + 1);
+        const int n = launch_backward_micro(mb, s);
+        if (n == 0) return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
+                                                cudaGetErrorString(cudaGetLastError()));
+        g_launches += n;
+      }
+    } else if (l >= tail_from) {
       tail->layer[tail->n++] = a;
       if (l == tail_from) {
         const LayerDesc& d0 = p->layers[tail_from];
-        const LayerDesc& dl = p->layers[p->L - 1];
+        const LayerDesc& dl = p->layers[microb_from - 1];
         tail->pf_ptr[0] = p->d_tpar + d0.e_base;
         tail->pf_bytes[0] = (dl.e_base + dl.E - d0.e_base) * (long long)sizeof(int);
         tail->pf_ptr[1] = p->d_toff + d0.toff_base;
@@ -1074,7 +1134,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
         if (n == 0) return fail(KLAY_ECUDA, std::string("tail launch failed: ") +
                                                 cudaGetErrorString(cudaGetLastError()));
         g_launches += n;
-        if (g_tail_trace) tail_trace_dump("backward", p->L - tail_from);
+        if (g_tail_trace) tail_trace_dump("backward", microb_from - tail_from);
       }
     } else {
       int mode = BW_PASS_;

@@ -89,6 +89,25 @@ struct MicroArgs {
   long long ld;
   T eps;
 };
+// backward micro tail (log semiring): steps i = 0.. walk the micro layers top
+// down; step i computes the children's adjoints of one layer
+template <typename T>
+struct MicroBwdArgs {
+  const T* gin;                     // adjoint rows of the top layer (seeded)
+  T* gout[MICRO_MAX_LAYERS];        // children's adjoint rows per step (null: not stored)
+  const T* vpar[MICRO_MAX_LAYERS];  // forward values of the parents / children
+  const T* vchild[MICRO_MAX_LAYERS];
+  int wp[MICRO_MAX_LAYERS];         // parents (layer width) / children (width below)
+  int wc[MICRO_MAX_LAYERS];
+  int csr_at[MICRO_MAX_LAYERS];     // [wc+1 transposed offsets, E parent indices] in csr
+  int logsum[MICRO_MAX_LAYERS];     // sum layer (weighted edges) / product layer (pass)
+  const int* csr;
+  int csr_ints;
+  int n, w_top, V, unary_ok;
+  long long ld;
+};
+int launch_backward_micro(const MicroBwdArgs<float>& m, cudaStream_t s);
+int launch_backward_micro(const MicroBwdArgs<double>& m, cudaStream_t s);
 int launch_forward_micro(int sr, const MicroArgs<float>& m, cudaStream_t s);
 int launch_forward_micro(int sr, const MicroArgs<double>& m, cudaStream_t s);
 int launch_forward_micro_u1(const MicroArgs<unsigned>& m, cudaStream_t s);

@@ -203,21 +203,27 @@ struct BwdGather {
     for (int c = 0; c < Vec<T>::N; ++c) r.v[c] = isfinite(x.v[c]) ? g.v[c] : g.v[c] * T(0);
     return r;
   }
+  // g[parent] * exp(child - parent); NaN/inf weights -> 0 (engine.py:346-352).
+  // (Unary parents never get here: their edges are flagged, see unary().
+  // A child equal to its parent gets exp(0) = 1 exactly, so no special
+  // case: one uniform path, no lane divergence.)
+  __device__ __forceinline__ static Vec<T> logsum_edge(const Vec<T>& g, const Vec<T>& P,
+                                                       const Vec<T>& x) {
+    Vec<T> r;
+#pragma unroll
+    for (int c = 0; c < Vec<T>::N; ++c) {
+      T w = kexp(x.v[c] - P.v[c]);
+      w = isfinite(w) ? w : T(0);
+      r.v[c] = g.v[c] * w;
+    }
+    return r;
+  }
   __device__ __forceinline__ Vec<T> combine(const Vec<T>& g, const Vec<T>& P, int row,
                                             const Vec<T>& x) const {
     constexpr int N = Vec<T>::N;
     Vec<T> r;
     if constexpr (MODE == BW_LOGSUM) {
-      // g[parent] * exp(child - parent); NaN/inf weights -> 0 (engine.py:346-352).
-      // (Unary parents never get here: their edges are flagged, see unary().
-      // A child equal to its parent gets exp(0) = 1 exactly, so no special
-      // case: one uniform path, no lane divergence.)
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        T w = kexp(x.v[c] - P.v[c]);
-        w = isfinite(w) ? w : T(0);
-        r.v[c] = g.v[c] * w;
-      }
+      r = logsum_edge(g, P, x);
     } else {
       // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
       // child gets g * (product of nonzero siblings) iff it is the only zero,
@@ -1062,6 +1068,124 @@ inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   cfg.gridDim = dim3((unsigned)((m.V + 32 * NV - 1) / (32 * NV)), 1, 1);
   cfg.blockDim = dim3(MICRO_WARPS * 32, 1, 1);
   cfg.dynamicSmemBytes = MICRO_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, m) == cudaSuccess ? 1 : 0;
+}
+
+// ---- backward micro tail (log semiring) ---------------------------------------
+//
+// The same idea for the adjoints of the thinnest layers: one CTA per 256-byte
+// column chunk (two workers per warp, one per half-warp, each reducing its own
+// child node) keeps the adjoint rows of two layers (ping-pong) and, for a
+// log-sum layer, the forward values of its parents and children in shared
+// memory. Layers alternate product / sum, so the values a sum layer needs are
+// fetched with cp.async while the product layer above it runs. Every child's
+// adjoint is summed over its parents in transposed-CSR order (x0 + sequential
+// rest, fan-out <= MICRO_FAN), edge weights as BwdGather: pass-through for a
+// product layer, g * exp(child - parent) for a sum layer.
+
+constexpr int MICROB_WARPS = 16;
+constexpr int MICROB_P = 16;  // 16-byte pieces per row chunk (256 bytes)
+constexpr size_t MICROB_SET = (size_t)MICRO_W * MICROB_P;  // pieces per row set
+constexpr size_t MICROB_SMEM = 4 * MICROB_SET * 16 + (size_t)MICRO_CSR * sizeof(int);
+
+template <typename T>
+__device__ __forceinline__ Vec<T> lds1(const uint4* p) {
+  Vec<T> r;
+  const uint4 u = *p;
+  memcpy(&r.v[0], &u, 16);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void sts1(uint4* p, const Vec<T>& r) {
+  uint4 u;
+  memcpy(&u, &r.v[0], 16);
+  *p = u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(MICROB_WARPS * 32, 1)
+    micro_bwd_kernel(const __grid_constant__ MicroBwdArgs<T> m) {
+  static_assert(NV == 1, "the backward micro tail assumes one 16-byte piece per lane");
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint4* gset[2] = {reinterpret_cast<uint4*>(smem), reinterpret_cast<uint4*>(smem) + MICROB_SET};
+  uint4* vp = reinterpret_cast<uint4*>(smem) + 2 * MICROB_SET;  // parent values
+  uint4* vx = reinterpret_cast<uint4*>(smem) + 3 * MICROB_SET;  // child values
+  int* csr = reinterpret_cast<int*>(smem + 4 * MICROB_SET * 16);
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const int worker = (threadIdx.x >> 5) * 2 + (lane >> 4);
+  constexpr int NW = MICROB_WARPS * 2;
+  const int vb = blockIdx.x * MICROB_P + hl;
+  const bool in_row = vb < m.V;
+  const size_t col = (size_t)(in_row ? vb : 0) * PIECE<T>;
+  const long long ld = m.ld;
+  for (int i = threadIdx.x; i < m.csr_ints; i += blockDim.x) csr[i] = __ldg(m.csr + i);
+#ifndef KLAY_NO_GDC
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+  // values of step i's parents / children into vp / vx (cp.async, not waited)
+  auto fetch_values = [&](int i) {
+    for (int r = worker; r < m.wp[i]; r += NW) cp_async16(vp + r * MICROB_P + hl, m.vpar[i] + r * ld + col);
+    for (int r = worker; r < m.wc[i]; r += NW) cp_async16(vx + r * MICROB_P + hl, m.vchild[i] + r * ld + col);
+    cp_async_commit();
+  };
+  for (int r = worker; r < m.w_top; r += NW) cp_async16(gset[0] + r * MICROB_P + hl, m.gin + r * ld + col);
+  cp_async_commit();
+  if (m.n > 0 && m.logsum[0]) fetch_values(0);
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int i = 0; i < m.n; ++i) {
+    const bool logsum = m.logsum[i] != 0;
+    if (!logsum && i + 1 < m.n && m.logsum[i + 1]) fetch_values(i + 1);
+    const uint4* src = gset[i & 1];
+    uint4* dst = gset[(i + 1) & 1];
+    const int* off = csr + m.csr_at[i];
+    const int* idx = off + m.wc[i] + 1;
+    T* out = m.gout[i];
+    for (int c = worker; c < m.wc[i]; c += NW) {
+      const int e0 = off[c], n = off[c + 1] - e0;
+      Vec<T> x{};
+      if (logsum) x = lds1<T>(vx + c * MICROB_P + hl);
+      auto val = [&](int e) {
+        const int row = idx[e0 + e];
+        const int p = row & 0x7fffffff;
+        const Vec<T> g = lds1<T>(src + p * MICROB_P + hl);
+        if (!logsum) return g;
+        if (row < 0 && m.unary_ok) return BwdGather<T, BW_LOGSUM>::unary(g, x);
+        return BwdGather<T, BW_LOGSUM>::logsum_edge(g, lds1<T>(vp + p * MICROB_P + hl), x);
+      };
+      Vec<T> r = val(0);
+      if (n > 1) {
+        Vec<T> acc = val(1);
+        for (int j = 2; j < n; ++j) acc = vadd(acc, val(j));
+        r = vadd(r, acc);
+      }
+      sts1(dst + c * MICROB_P + hl, r);
+      if (out && in_row) stv(out + (size_t)c * ld + col, r, 1);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
+template <typename T>
+inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
+  auto kern = micro_bwd_kernel<T>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MICROB_SMEM);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((m.V + MICROB_P - 1) / MICROB_P), 1, 1);
+  cfg.blockDim = dim3(MICROB_WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = MICROB_SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

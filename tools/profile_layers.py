@@ -63,8 +63,9 @@ def main():
     fwd_b, bwd_b = layer_bytes(tc, s, B, args.domain)
     peak, _ = load_peaks()
     widths = [tc.num_inputs] + [l.width for l in tc.layers]
-    tot = {k: [0, 0] for k in range(7)}
+    tot = {k: [0, 0] for k in range(8)}
     micro_l = min([l for (k, l) in acc if k == 6], default=len(tc.layers) + 1)
+    microb_l = min([l for (k, l) in acc if k == 7], default=len(tc.layers) + 1)
     print(f"{'kind':>4} {'l':>3} {'op':>4} {'Wprev':>6} {'W':>6} {'E':>7} {'us':>9} {'GB/s':>8} {'frac':>6}")
     for (k, l), ts in sorted(acc.items(), key=lambda kv: (kv[0][0], kv[0][1])):
         t = float(np.median(ts))
@@ -76,16 +77,17 @@ def main():
             gbs = b / (t / 1e3) / 1e9
             print(f"{k:>4} {l:>3} {op:>4} {widths[l-1]:>6} {widths[l]:>6} "
                   f"{len(tc.layers[l-1].sources):>7} {t*1e3:>9.1f} {gbs:>8.0f} {gbs/peak:>6.3f}")
-        elif k in (4, 5, 6):
-            layers = range(l, (micro_l if k == 4 else len(tc.layers) + 1))
-            b = sum((bwd_b if k == 5 else fwd_b)[i] for i in layers)
+        elif k in (4, 5, 6, 7):
+            top = micro_l if k == 4 else (microb_l if k == 5 else len(tc.layers) + 1)
+            layers = range(l, top)
+            b = sum((bwd_b if k in (5, 7) else fwd_b)[i] for i in layers)
             tot[k][1] += b
             gbs = b / (t / 1e3) / 1e9
             print(f"{k:>4} {l:>3} tail({len(layers)} layers) {t*1e3:>9.1f} us {gbs:>8.0f} GB/s")
         else:
             print(f"{k:>4} {l:>3} boundary {t*1e3:>9.1f} us")
     for k, name in ((0, "fwd"), (1, "bwd"), (2, "fwd-boundary"), (3, "bwd-boundary"),
-                    (4, "fwd-tail"), (5, "bwd-tail"), (6, "fwd-micro-tail")):
+                    (4, "fwd-tail"), (5, "bwd-tail"), (6, "fwd-micro-tail"), (7, "bwd-micro-tail")):
         t, b = tot[k]
         if t:
             print(f"{name}: {t:.3f} ms, {b/1e9:.3f} GB algorithmic, "
