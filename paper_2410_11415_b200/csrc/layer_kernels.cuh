@@ -970,32 +970,37 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
 //
 // Above the persistent tail's layers the circuit narrows to a few dozen
 // nodes; there a layer is latency, not bandwidth: a cluster barrier plus an
-// L2 round trip per layer. One CTA per 512-byte column chunk holds two
-// layers' rows of its chunk in shared memory (ping-pong), reduces each node
-// from shared memory, stores the result to both shared memory and the trace,
-// and meets the other warps of the CTA at a __syncthreads per layer. The CSR
-// of all micro layers is staged once, before the PDL wait.
+// L2 round trip per layer. One CTA per 256-byte column chunk holds two
+// layers' rows of its chunk in shared memory (ping-pong); each half-warp is a
+// worker that reduces one node from shared memory, stores the result to both
+// shared memory and the trace, and the CTA meets at a __syncthreads per
+// layer. The CSR of all micro layers is staged once, before the PDL wait.
 
 constexpr int MICRO_WARPS = 16;
-constexpr size_t MICRO_ROWS_BYTES = (size_t)2 * MICRO_W * NV * 32 * 16;
-constexpr size_t MICRO_SMEM = MICRO_ROWS_BYTES + (size_t)MICRO_CSR * sizeof(int);
+constexpr int MICRO_P = 16;  // 16-byte pieces per row chunk (256 bytes)
+constexpr size_t MICRO_SET = (size_t)MICRO_W * MICRO_P;  // pieces per row set
+constexpr size_t MICRO_SMEM = 2 * MICRO_SET * 16 + (size_t)MICRO_CSR * sizeof(int);
 
 template <typename T>
-__device__ __forceinline__ void sts_vec(uint4* slot, const Vec<T>& r, int lane) {
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    uint4 u;
-    memcpy(&u, &r.v[q * PIECE<T>], 16);
-    slot[q * 32 + lane] = u;
-  }
+__device__ __forceinline__ Vec<T> lds1(const uint4* p) {
+  Vec<T> r;
+  const uint4 u = *p;
+  memcpy(&r.v[0], &u, 16);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void sts1(uint4* p, const Vec<T>& r) {
+  uint4 u;
+  memcpy(&u, &r.v[0], 16);
+  *p = u;
 }
 
-// one node over rows in shared memory, in the reference's order (n <= MICRO_FAN:
-// numpy's pairwise sum is x0 + sequential sum of the rest)
+// one node over rows in shared memory (`rows` at the worker's piece), in the
+// reference's order (n <= MICRO_FAN: numpy's pairwise sum is x0 + sequential
+// sum of the rest)
 template <typename T, int RK>
-__device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, const int* idx, int n, int lane,
-                                               T eps) {
-  auto v = [&](int e) { return lds_vec<T>(rows + (size_t)idx[e] * 32 * NV, lane); };
+__device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, const int* idx, int n, T eps) {
+  auto v = [&](int e) { return lds1<T>(rows + (size_t)idx[e] * MICRO_P); };
   Vec<T> out = v(0);
   if constexpr (RK == RK_SUM) {
     if (n > 1) {
@@ -1023,34 +1028,39 @@ __device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, const int* idx
 template <typename T, int RKP, int RKS>
 __global__ void __launch_bounds__(MICRO_WARPS * 32, 1)
     micro_kernel(const __grid_constant__ MicroArgs<T> m) {
+  static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* rows = reinterpret_cast<uint4*>(smem);
-  int* csr = reinterpret_cast<int*>(smem + MICRO_ROWS_BYTES);
-  constexpr size_t RV = (size_t)MICRO_W * NV * 32;  // pieces per row buffer
-  const int chunk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < m.csr_ints; i += blockDim.x) csr[i] = __ldg(m.csr + i);
-  const LaneCols lc = lane_cols<T>(m.V, chunk, lane);
+  int* csr = reinterpret_cast<int*>(smem + 2 * MICRO_SET * 16);
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const int worker = (threadIdx.x >> 5) * 2 + (lane >> 4);
+  constexpr int NW = MICRO_WARPS * 2;
+  const int vb = blockIdx.x * MICRO_P + hl;
+  const bool in_row = vb < m.V;
+  const size_t col = (size_t)(in_row ? vb : 0) * PIECE<T>;
   const long long ld = m.ld;
+  for (int i = threadIdx.x; i < m.csr_ints; i += blockDim.x) csr[i] = __ldg(m.csr + i);
 #ifndef KLAY_NO_GDC
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #endif
-  for (int r = warp; r < m.w_in; r += MICRO_WARPS)
-    sts_vec(rows + (size_t)r * NV * 32, ldv(m.in + (size_t)r * ld + lc.col, lc.nl), lane);
+  for (int r = worker; r < m.w_in; r += NW) cp_async16(rows + r * MICRO_P + hl, m.in + r * ld + col);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   for (int i = 0; i < m.n; ++i) {
-    const uint4* src = rows + (i & 1) * RV;
-    uint4* dst = rows + ((i + 1) & 1) * RV;
+    const uint4* src = rows + (i & 1) * MICRO_SET;
+    uint4* dst = rows + ((i + 1) & 1) * MICRO_SET;
     const int* off = csr + m.csr_at[i];
     const int* idx = off + m.w[i] + 1;
     T* out = m.out[i];
     const bool prod = m.prod[i] != 0;
-    for (int nd = warp; nd < m.w[i]; nd += MICRO_WARPS) {
+    for (int nd = worker; nd < m.w[i]; nd += NW) {
       const int e0 = off[nd], n = off[nd + 1] - e0;
-      const Vec<T> r = prod ? micro_reduce<T, RKP>(src, idx + e0, n, lane, m.eps)
-                            : micro_reduce<T, RKS>(src, idx + e0, n, lane, m.eps);
-      sts_vec(dst + (size_t)nd * NV * 32, r, lane);
-      if (out) stv(out + (size_t)nd * ld + lc.col, r, lc.na);
+      const Vec<T> r = prod ? micro_reduce<T, RKP>(src + hl, idx + e0, n, m.eps)
+                            : micro_reduce<T, RKS>(src + hl, idx + e0, n, m.eps);
+      sts1(dst + nd * MICRO_P + hl, r);
+      if (out && in_row) stv(out + (size_t)nd * ld + col, r, 1);
     }
     __syncthreads();
   }
@@ -1065,7 +1075,7 @@ inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((m.V + 32 * NV - 1) / (32 * NV)), 1, 1);
+  cfg.gridDim = dim3((unsigned)((m.V + MICRO_P - 1) / MICRO_P), 1, 1);
   cfg.blockDim = dim3(MICRO_WARPS * 32, 1, 1);
   cfg.dynamicSmemBytes = MICRO_SMEM;
   cfg.stream = s;
@@ -1090,23 +1100,10 @@ inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
 // product layer, g * exp(child - parent) for a sum layer.
 
 constexpr int MICROB_WARPS = 16;
-constexpr int MICROB_P = 16;  // 16-byte pieces per row chunk (256 bytes)
-constexpr size_t MICROB_SET = (size_t)MICRO_W * MICROB_P;  // pieces per row set
+constexpr int MICROB_P = MICRO_P;
+constexpr size_t MICROB_SET = MICRO_SET;
 constexpr size_t MICROB_SMEM = 4 * MICROB_SET * 16 + (size_t)MICRO_CSR * sizeof(int);
 
-template <typename T>
-__device__ __forceinline__ Vec<T> lds1(const uint4* p) {
-  Vec<T> r;
-  const uint4 u = *p;
-  memcpy(&r.v[0], &u, 16);
-  return r;
-}
-template <typename T>
-__device__ __forceinline__ void sts1(uint4* p, const Vec<T>& r) {
-  uint4 u;
-  memcpy(&u, &r.v[0], 16);
-  *p = u;
-}
 
 template <typename T>
 __global__ void __launch_bounds__(MICROB_WARPS * 32, 1)
