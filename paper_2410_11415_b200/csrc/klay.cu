@@ -328,14 +328,12 @@ struct KlayPlan {
   int64_t n_alias = 0;
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
   int32_t tail_from = 0;  // first layer of the persistent tail (L = no tail)
-  int32_t micro_from = 0;  // first layer of the forward micro tail (>= tail_from; L = none)
-  std::vector<int> micro_at;  // per micro layer: offset of its CSR in d_micro
-  int* d_micro = nullptr;     // packed micro-tail CSR ([W+1] local offsets, [E] indices per layer)
-  int micro_ints = 0;
-  int32_t microb_from = 0;  // first layer of the backward micro tail (>= tail_from; L = none)
-  std::vector<int> microb_at;  // per layer from microb_from: offset of its transposed CSR
+  int32_t micro_from = 0;  // first layer of the forward micro tail (L = none)
+  std::vector<int> micro_at, micro_n;  // per micro layer: offset / length of its CSR in d_micro
+  int* d_micro = nullptr;  // packed micro-tail CSR ([W+1] local offsets, [E] indices per layer)
+  int32_t microb_from = 0;  // first layer of the backward micro tail (L = none)
+  std::vector<int> microb_at, microb_n;  // per layer from microb_from: its transposed CSR
   int* d_microb = nullptr;
-  int microb_ints = 0;
 };
 
 extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
@@ -395,7 +393,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
                           std::vector<int>& aoff, std::vector<int>& aidx, std::vector<int>& omap,
                           std::vector<int2>& pairs, AddSet add_set) {
   const int L = p->L;
-  const int tail = p->tail_from;
+  // nodes read by a tail (persistent or micro) are never aliased
+  const int tail = std::min({p->tail_from, p->micro_from, p->microb_from});
   auto width = [&](int nl) -> int64_t { return nl == 0 ? K : widths[nl - 1]; };
   auto is_sum = [](int nl) { return nl >= 1 && ((nl - 1) % 2 == 1); };
   std::vector<std::vector<int>> child(L + 1), npar(L + 1), par(L + 1), up(L + 1), srow(L + 1),
@@ -724,57 +723,40 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   }
   p->total_rows = row;
   p->WL = prev_w;
-  // forward micro tail: the longest suffix of tail layers that fit it
-  // (widths and fan-ins bounded, CSR inside MICRO_CSR ints)
-  std::vector<int> micro;
-  {
+  // micro tails: the longest suffix of layers that fit them (widths, fan-in
+  // (forward) / fan-out (backward) and one layer's CSR bounded); a layer's
+  // CSR block starts 16-byte aligned for the per-layer cp.async staging
+  auto micro_suffix = [&](bool fwd, std::vector<int>& packed, std::vector<int>& at,
+                          std::vector<int>& len) -> int32_t {
     int32_t mf = num_layers;
-    int64_t ints = 0;
-    while (mf > tail_from && num_layers - mf < MICRO_MAX_LAYERS) {
+    while (mf > 0 && num_layers - mf < MICRO_MAX_LAYERS) {
       const LayerDesc& d = p->layers[mf - 1];
+      const std::vector<int>& o = fwd ? off : toff;
+      const int64_t base = fwd ? d.off_base : d.toff_base, nodes = fwd ? d.W : d.Wprev;
       int maxfan = 0;
-      for (int64_t i = 0; i < d.W; ++i)
-        maxfan = std::max(maxfan, off[d.off_base + i + 1] - off[d.off_base + i]);
-      if (d.W > MICRO_W || d.Wprev > MICRO_W || maxfan > MICRO_FAN ||
-          ints + d.W + 1 + d.E > MICRO_CSR)
+      for (int64_t i = 0; i < nodes; ++i) maxfan = std::max(maxfan, o[base + i + 1] - o[base + i]);
+      if (d.W > MICRO_W || d.Wprev > MICRO_W || maxfan > MICRO_FAN || nodes + 1 + d.E > MICRO_CSR)
         break;
-      ints += d.W + 1 + d.E;
       --mf;
     }
-    p->micro_from = mf;
     for (int32_t l = mf; l < num_layers; ++l) {
       const LayerDesc& d = p->layers[l];
-      p->micro_at.push_back((int)micro.size());
-      for (int64_t i = 0; i <= d.W; ++i) micro.push_back(off[d.off_base + i]);
-      for (int64_t e = 0; e < d.E; ++e) micro.push_back(src[d.e_base + e]);
+      at.push_back((int)packed.size());
+      if (fwd) {
+        for (int64_t i = 0; i <= d.W; ++i) packed.push_back(off[d.off_base + i]);
+        for (int64_t e = 0; e < d.E; ++e) packed.push_back(src[d.e_base + e]);
+      } else {
+        for (int64_t j = 0; j <= d.Wprev; ++j) packed.push_back(toff[d.toff_base + j]);
+        for (int64_t e = 0; e < d.E; ++e) packed.push_back(tpar[d.e_base + e]);
+      }
+      len.push_back((int)packed.size() - at.back());
+      while (packed.size() % 4) packed.push_back(0);
     }
-    p->micro_ints = (int)micro.size();
-  }
-  // backward micro tail: the same over the transposed CSR (fan-out bounded)
-  std::vector<int> microb;
-  {
-    int32_t mf = num_layers;
-    int64_t ints = 0;
-    while (mf > tail_from && num_layers - mf < MICRO_MAX_LAYERS) {
-      const LayerDesc& d = p->layers[mf - 1];
-      int maxfan = 0;
-      for (int64_t j = 0; j < d.Wprev; ++j)
-        maxfan = std::max(maxfan, toff[d.toff_base + j + 1] - toff[d.toff_base + j]);
-      if (d.W > MICRO_W || d.Wprev > MICRO_W || maxfan > MICRO_FAN ||
-          ints + d.Wprev + 1 + d.E > MICRO_CSR)
-        break;
-      ints += d.Wprev + 1 + d.E;
-      --mf;
-    }
-    p->microb_from = mf;
-    for (int32_t l = mf; l < num_layers; ++l) {
-      const LayerDesc& d = p->layers[l];
-      p->microb_at.push_back((int)microb.size());
-      for (int64_t j = 0; j <= d.Wprev; ++j) microb.push_back(toff[d.toff_base + j]);
-      for (int64_t e = 0; e < d.E; ++e) microb.push_back(tpar[d.e_base + e]);
-    }
-    p->microb_ints = (int)microb.size();
-  }
+    return mf;
+  };
+  std::vector<int> micro, microb;
+  p->micro_from = micro_suffix(true, micro, p->micro_at, p->micro_n);
+  p->microb_from = micro_suffix(false, microb, p->microb_at, p->microb_n);
   if (num_layers >= 2 && row < (1LL << 30)) {
     build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
                   alias_rows,
@@ -972,6 +954,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       micro.out[i] = (retain || l == p->L - 1) ? cur : nullptr;
       micro.w[i] = (int)d.W;
       micro.csr_at[i] = p->micro_at[l - p->micro_from];
+      micro.csr_n[i] = p->micro_n[l - p->micro_from];
       micro.prod[i] = d.prod ? 1 : 0;
     } else if (l >= tail_from) {
       tail->layer[tail->n++] = a;
@@ -1012,7 +995,6 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   }
   if (micro.n > 0) {
     micro.csr = p->d_micro;
-    micro.csr_ints = p->micro_ints;
     micro.V = V;
     micro.ld = ld;
     micro.eps = (T)eps;
@@ -1097,10 +1079,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       mb.wp[i] = (int)d.W;
       mb.wc[i] = (int)d.Wprev;
       mb.csr_at[i] = p->microb_at[l - p->microb_from];
+      mb.csr_n[i] = p->microb_n[l - p->microb_from];
       mb.logsum[i] = d.prod ? 0 : 1;
       if (l == microb_from) {
         mb.csr = p->d_microb;
-        mb.csr_ints = p->microb_ints;
         mb.V = V;
         mb.ld = ld;
         mb.unary_ok = a.unary_ok;

@@ -68,13 +68,14 @@ struct TailArgs {
   unsigned long long* trace_ts;  // KLAY_TAIL_TRACE=1: per-layer globaltimer stamps (debug)
 };
 
-// The forward micro tail: the thinnest top layers (every width <= MICRO_W,
-// fan-in <= MICRO_FAN) evaluated by one CTA per column chunk with the layer
-// values held in shared memory; CSR offsets (local, from 0) and indices of
-// every micro layer are packed into one int block staged in shared memory.
+// The micro tails: the thin top layers (every width <= MICRO_W, fan-in /
+// fan-out <= MICRO_FAN, one layer's CSR <= MICRO_CSR ints) evaluated by one
+// CTA per column chunk with the layer values held in shared memory. Each
+// layer's CSR (offsets local from 0, then indices) is packed at a 16-byte
+// aligned offset of one plan int array and staged per layer.
 constexpr int MICRO_MAX_LAYERS = 64;
-constexpr int MICRO_W = 192;
-constexpr int MICRO_FAN = 8;
+constexpr int MICRO_W = 1280;
+constexpr int MICRO_FAN = 129;
 constexpr int MICRO_CSR = 4096;  // ints
 template <typename T>
 struct MicroArgs {
@@ -82,9 +83,9 @@ struct MicroArgs {
   T* out[MICRO_MAX_LAYERS];       // output rows per layer (null: not stored)
   int w[MICRO_MAX_LAYERS];        // widths
   int csr_at[MICRO_MAX_LAYERS];   // offset of the layer's [W+1 offsets, E indices] in csr
+  int csr_n[MICRO_MAX_LAYERS];    // its length (ints)
   int prod[MICRO_MAX_LAYERS];
   const int* csr;
-  int csr_ints;
   int n, w_in, V;
   long long ld;
   T eps;
@@ -100,9 +101,9 @@ struct MicroBwdArgs {
   int wp[MICRO_MAX_LAYERS];         // parents (layer width) / children (width below)
   int wc[MICRO_MAX_LAYERS];
   int csr_at[MICRO_MAX_LAYERS];     // [wc+1 transposed offsets, E parent indices] in csr
+  int csr_n[MICRO_MAX_LAYERS];
   int logsum[MICRO_MAX_LAYERS];     // sum layer (weighted edges) / product layer (pass)
   const int* csr;
-  int csr_ints;
   int n, w_top, V, unary_ok;
   long long ld;
 };

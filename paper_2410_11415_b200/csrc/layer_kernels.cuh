@@ -966,20 +966,35 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, t) == cudaSuccess ? 1 : 0;
 }
 
-// ---- micro tail: the thinnest layers with their values in shared memory ----
+// ---- micro tail: the thin upper layers with their values in shared memory ----
 //
-// Above the persistent tail's layers the circuit narrows to a few dozen
-// nodes; there a layer is latency, not bandwidth: a cluster barrier plus an
-// L2 round trip per layer. One CTA per 256-byte column chunk holds two
-// layers' rows of its chunk in shared memory (ping-pong); each half-warp is a
-// worker that reduces one node from shared memory, stores the result to both
-// shared memory and the trace, and the CTA meets at a __syncthreads per
-// layer. The CSR of all micro layers is staged once, before the PDL wait.
+// Above the bandwidth-bound layers the circuit narrows to a few thousand
+// nodes and less; there a layer is latency, not bandwidth: a launch (or a
+// cluster barrier) plus dependent L2 round trips per layer. The micro tails
+// run all of those layers in one launch of independent CTAs, one per column
+// chunk of P 16-byte pieces: a worker of P lanes reduces one node at a time
+// over rows held in shared memory, and the CTA meets at one __syncthreads
+// per layer. The next layer's CSR (plan data) is staged with cp.async while
+// the current layer runs.
+//
+// Forward (any semiring): two layers' value rows (ping-pong); each result
+// goes to shared memory and to the trace. Backward (log semiring): two
+// layers' adjoint rows plus, for a log-sum layer, the forward values of its
+// parents and children, fetched with cp.async while the product layer above
+// it runs (layers alternate product / sum). Only the lowest layer's adjoints
+// leave the CTA.
+//
+// Reductions follow the reference's order exactly: x0 + numpy's pairwise sum
+// of the rest (fan-in <= MICRO_FAN = PW_BLOCK + 1: one pairwise block),
+// sequential products / max / min, the streaming logsumexp of LseOp.
 
-constexpr int MICRO_WARPS = 16;
-constexpr int MICRO_P = 16;  // 16-byte pieces per row chunk (256 bytes)
-constexpr size_t MICRO_SET = (size_t)MICRO_W * MICRO_P;  // pieces per row set
-constexpr size_t MICRO_SMEM = 2 * MICRO_SET * 16 + (size_t)MICRO_CSR * sizeof(int);
+constexpr int MICRO_THREADS = 512;
+constexpr int MICRO_PF = 4;  // forward: 64-byte column chunks
+constexpr int MICRO_PB = 2;  // backward: 32-byte column chunks (four row sets)
+template <int P>
+constexpr size_t micro_smem(int sets) {
+  return (size_t)sets * MICRO_W * P * 16 + (size_t)2 * MICRO_CSR * sizeof(int);
+}
 
 template <typename T>
 __device__ __forceinline__ Vec<T> lds1(const uint4* p) {
@@ -995,73 +1010,103 @@ __device__ __forceinline__ void sts1(uint4* p, const Vec<T>& r) {
   *p = u;
 }
 
-// one node over rows in shared memory (`rows` at the worker's piece), in the
-// reference's order (n <= MICRO_FAN: numpy's pairwise sum is x0 + sequential
-// sum of the rest)
-template <typename T, int RK>
-__device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, const int* idx, int n, T eps) {
-  auto v = [&](int e) { return lds1<T>(rows + (size_t)idx[e] * MICRO_P); };
+// x0 + pairwise(x1 .. x_{n-1}) for n <= PW_BLOCK + 1, numpy's order
+// (sequential below 8 elements, else 8 interleaved accumulators)
+template <typename T, typename F>
+__device__ __forceinline__ Vec<T> micro_sum(int n, F&& v) {
   Vec<T> out = v(0);
+  const int m = n - 1;
+  if (m <= 0) return out;
+  if (m < 8) {
+    Vec<T> acc = v(1);
+    for (int j = 2; j < n; ++j) acc = vadd(acc, v(j));
+    return vadd(out, acc);
+  }
+  Vec<T> r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = v(1 + j);
+  const int mainend = m - (m & 7);
+  int i = 8;
+  for (; i < mainend; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = vadd(r[j], v(1 + i + j));
+  }
+  Vec<T> res = combine8(r);
+  for (; i < m; ++i) res = vadd(res, v(1 + i));
+  return vadd(out, res);
+}
+
+template <typename T, int RK>
+__device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, int P, const int* idx, int n, T eps) {
+  auto v = [&](int e) { return lds1<T>(rows + (size_t)idx[e] * P); };
   if constexpr (RK == RK_SUM) {
-    if (n > 1) {
-      Vec<T> acc = v(1);
-      for (int j = 2; j < n; ++j) acc = vadd(acc, v(j));
-      out = vadd(out, acc);
-    }
+    return micro_sum<T>(n, v);
   } else if constexpr (RK == RK_LSE) {
+    Vec<T> out = v(0);
     if (n > 1 || eps != T(0)) {
       LseOp<T> op;
       op.eps = eps;
       op.begin(n);
       op.push(out);
       for (int j = 1; j < n; ++j) op.push(v(j));
-      out = op.result();
-    } else {
-      out = lse_unary(out);
+      return op.result();
     }
+    return lse_unary(out);
   } else {
+    Vec<T> out = v(0);
     for (int j = 1; j < n; ++j) seq_combine<T, RK>(out, v(j));
+    return out;
   }
-  return out;
+}
+
+// stage `n` ints of plan CSR (16-byte aligned) into shared memory; not waited
+__device__ __forceinline__ void micro_stage_csr(int* dst, const int* src, int n) {
+  for (int i = threadIdx.x; i < (n + 3) / 4; i += blockDim.x) cp_async16(dst + 4 * i, src + 4 * i);
 }
 
 template <typename T, int RKP, int RKS>
-__global__ void __launch_bounds__(MICRO_WARPS * 32, 1)
+__global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_kernel(const __grid_constant__ MicroArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
+  constexpr int P = MICRO_PF, NW = MICRO_THREADS / P;
+  constexpr size_t SET = (size_t)MICRO_W * P;
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* rows = reinterpret_cast<uint4*>(smem);
-  int* csr = reinterpret_cast<int*>(smem + 2 * MICRO_SET * 16);
-  const int lane = threadIdx.x & 31, hl = lane & 15;
-  const int worker = (threadIdx.x >> 5) * 2 + (lane >> 4);
-  constexpr int NW = MICRO_WARPS * 2;
-  const int vb = blockIdx.x * MICRO_P + hl;
+  int* csr = reinterpret_cast<int*>(smem + 2 * SET * 16);
+  const int hl = threadIdx.x % P, worker = threadIdx.x / P;
+  const int vb = blockIdx.x * P + hl;
   const bool in_row = vb < m.V;
   const size_t col = (size_t)(in_row ? vb : 0) * PIECE<T>;
   const long long ld = m.ld;
-  for (int i = threadIdx.x; i < m.csr_ints; i += blockDim.x) csr[i] = __ldg(m.csr + i);
+  micro_stage_csr(csr, m.csr + m.csr_at[0], m.csr_n[0]);
+  cp_async_commit();
 #ifndef KLAY_NO_GDC
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #endif
-  for (int r = worker; r < m.w_in; r += NW) cp_async16(rows + r * MICRO_P + hl, m.in + r * ld + col);
+  for (int r = worker; r < m.w_in; r += NW) cp_async16(rows + r * P + hl, m.in + r * ld + col);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   for (int i = 0; i < m.n; ++i) {
-    const uint4* src = rows + (i & 1) * MICRO_SET;
-    uint4* dst = rows + ((i + 1) & 1) * MICRO_SET;
-    const int* off = csr + m.csr_at[i];
+    if (i + 1 < m.n) {
+      micro_stage_csr(csr + ((i + 1) & 1) * MICRO_CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
+      cp_async_commit();
+    }
+    const uint4* src = rows + (i & 1) * SET + hl;
+    uint4* dst = rows + ((i + 1) & 1) * SET;
+    const int* off = csr + (i & 1) * MICRO_CSR;
     const int* idx = off + m.w[i] + 1;
     T* out = m.out[i];
     const bool prod = m.prod[i] != 0;
     for (int nd = worker; nd < m.w[i]; nd += NW) {
       const int e0 = off[nd], n = off[nd + 1] - e0;
-      const Vec<T> r = prod ? micro_reduce<T, RKP>(src + hl, idx + e0, n, m.eps)
-                            : micro_reduce<T, RKS>(src + hl, idx + e0, n, m.eps);
-      sts1(dst + nd * MICRO_P + hl, r);
+      const Vec<T> r = prod ? micro_reduce<T, RKP>(src, P, idx + e0, n, m.eps)
+                            : micro_reduce<T, RKS>(src, P, idx + e0, n, m.eps);
+      sts1(dst + nd * P + hl, r);
       if (out && in_row) stv(out + (size_t)nd * ld + col, r, 1);
     }
+    cp_async_wait<0>();
     __syncthreads();
   }
 }
@@ -1069,15 +1114,16 @@ __global__ void __launch_bounds__(MICRO_WARPS * 32, 1)
 template <typename T, int RKP, int RKS>
 inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   auto kern = micro_kernel<T, RKP, RKS>;
+  constexpr size_t bytes = micro_smem<MICRO_PF>(2);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MICRO_SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((m.V + MICRO_P - 1) / MICRO_P), 1, 1);
-  cfg.blockDim = dim3(MICRO_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = MICRO_SMEM;
+  cfg.gridDim = dim3((unsigned)((m.V + MICRO_PF - 1) / MICRO_PF), 1, 1);
+  cfg.blockDim = dim3(MICRO_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1087,83 +1133,65 @@ inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, m) == cudaSuccess ? 1 : 0;
 }
 
-// ---- backward micro tail (log semiring) ---------------------------------------
-//
-// The same idea for the adjoints of the thinnest layers: one CTA per 256-byte
-// column chunk (two workers per warp, one per half-warp, each reducing its own
-// child node) keeps the adjoint rows of two layers (ping-pong) and, for a
-// log-sum layer, the forward values of its parents and children in shared
-// memory. Layers alternate product / sum, so the values a sum layer needs are
-// fetched with cp.async while the product layer above it runs. Every child's
-// adjoint is summed over its parents in transposed-CSR order (x0 + sequential
-// rest, fan-out <= MICRO_FAN), edge weights as BwdGather: pass-through for a
-// product layer, g * exp(child - parent) for a sum layer.
-
-constexpr int MICROB_WARPS = 16;
-constexpr int MICROB_P = MICRO_P;
-constexpr size_t MICROB_SET = MICRO_SET;
-constexpr size_t MICROB_SMEM = 4 * MICROB_SET * 16 + (size_t)MICRO_CSR * sizeof(int);
-
-
 template <typename T>
-__global__ void __launch_bounds__(MICROB_WARPS * 32, 1)
+__global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_bwd_kernel(const __grid_constant__ MicroBwdArgs<T> m) {
-  static_assert(NV == 1, "the backward micro tail assumes one 16-byte piece per lane");
+  static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
+  constexpr int P = MICRO_PB, NW = MICRO_THREADS / P;
+  constexpr size_t SET = (size_t)MICRO_W * P;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint4* gset[2] = {reinterpret_cast<uint4*>(smem), reinterpret_cast<uint4*>(smem) + MICROB_SET};
-  uint4* vp = reinterpret_cast<uint4*>(smem) + 2 * MICROB_SET;  // parent values
-  uint4* vx = reinterpret_cast<uint4*>(smem) + 3 * MICROB_SET;  // child values
-  int* csr = reinterpret_cast<int*>(smem + 4 * MICROB_SET * 16);
-  const int lane = threadIdx.x & 31, hl = lane & 15;
-  const int worker = (threadIdx.x >> 5) * 2 + (lane >> 4);
-  constexpr int NW = MICROB_WARPS * 2;
-  const int vb = blockIdx.x * MICROB_P + hl;
+  uint4* gset = reinterpret_cast<uint4*>(smem);              // [2] adjoint row sets
+  uint4* vp = reinterpret_cast<uint4*>(smem) + 2 * SET;      // parent values
+  uint4* vx = reinterpret_cast<uint4*>(smem) + 3 * SET;      // child values
+  int* csr = reinterpret_cast<int*>(smem + 4 * SET * 16);
+  const int hl = threadIdx.x % P, worker = threadIdx.x / P;
+  const int vb = blockIdx.x * P + hl;
   const bool in_row = vb < m.V;
   const size_t col = (size_t)(in_row ? vb : 0) * PIECE<T>;
   const long long ld = m.ld;
-  for (int i = threadIdx.x; i < m.csr_ints; i += blockDim.x) csr[i] = __ldg(m.csr + i);
+  micro_stage_csr(csr, m.csr + m.csr_at[0], m.csr_n[0]);
+  cp_async_commit();
 #ifndef KLAY_NO_GDC
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #endif
-  // values of step i's parents / children into vp / vx (cp.async, not waited)
+  // values of step i's parents / children into vp / vx (not waited)
   auto fetch_values = [&](int i) {
-    for (int r = worker; r < m.wp[i]; r += NW) cp_async16(vp + r * MICROB_P + hl, m.vpar[i] + r * ld + col);
-    for (int r = worker; r < m.wc[i]; r += NW) cp_async16(vx + r * MICROB_P + hl, m.vchild[i] + r * ld + col);
-    cp_async_commit();
+    for (int r = worker; r < m.wp[i]; r += NW) cp_async16(vp + r * P + hl, m.vpar[i] + r * ld + col);
+    for (int r = worker; r < m.wc[i]; r += NW) cp_async16(vx + r * P + hl, m.vchild[i] + r * ld + col);
   };
-  for (int r = worker; r < m.w_top; r += NW) cp_async16(gset[0] + r * MICROB_P + hl, m.gin + r * ld + col);
-  cp_async_commit();
+  for (int r = worker; r < m.w_top; r += NW) cp_async16(gset + r * P + hl, m.gin + r * ld + col);
   if (m.n > 0 && m.logsum[0]) fetch_values(0);
+  cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   for (int i = 0; i < m.n; ++i) {
     const bool logsum = m.logsum[i] != 0;
-    if (!logsum && i + 1 < m.n && m.logsum[i + 1]) fetch_values(i + 1);
-    const uint4* src = gset[i & 1];
-    uint4* dst = gset[(i + 1) & 1];
-    const int* off = csr + m.csr_at[i];
+    if (i + 1 < m.n) {
+      micro_stage_csr(csr + ((i + 1) & 1) * MICRO_CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
+      // a product layer leaves vp / vx free for the log-sum layer below
+      if (!logsum && m.logsum[i + 1]) fetch_values(i + 1);
+      cp_async_commit();
+    }
+    const uint4* src = gset + (i & 1) * SET + hl;
+    uint4* dst = gset + ((i + 1) & 1) * SET;
+    const int* off = csr + (i & 1) * MICRO_CSR;
     const int* idx = off + m.wc[i] + 1;
     T* out = m.gout[i];
     for (int c = worker; c < m.wc[i]; c += NW) {
       const int e0 = off[c], n = off[c + 1] - e0;
       Vec<T> x{};
-      if (logsum) x = lds1<T>(vx + c * MICROB_P + hl);
+      if (logsum) x = lds1<T>(vx + c * P + hl);
       auto val = [&](int e) {
         const int row = idx[e0 + e];
         const int p = row & 0x7fffffff;
-        const Vec<T> g = lds1<T>(src + p * MICROB_P + hl);
+        const Vec<T> g = lds1<T>(src + (size_t)p * P);
         if (!logsum) return g;
         if (row < 0 && m.unary_ok) return BwdGather<T, BW_LOGSUM>::unary(g, x);
-        return BwdGather<T, BW_LOGSUM>::logsum_edge(g, lds1<T>(vp + p * MICROB_P + hl), x);
+        return BwdGather<T, BW_LOGSUM>::logsum_edge(g, lds1<T>(vp + (size_t)p * P + hl), x);
       };
-      Vec<T> r = val(0);
-      if (n > 1) {
-        Vec<T> acc = val(1);
-        for (int j = 2; j < n; ++j) acc = vadd(acc, val(j));
-        r = vadd(r, acc);
-      }
-      sts1(dst + c * MICROB_P + hl, r);
+      const Vec<T> r = micro_sum<T>(n, val);
+      sts1(dst + c * P + hl, r);
       if (out && in_row) stv(out + (size_t)c * ld + col, r, 1);
     }
     cp_async_wait<0>();
@@ -1174,15 +1202,16 @@ __global__ void __launch_bounds__(MICROB_WARPS * 32, 1)
 template <typename T>
 inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
   auto kern = micro_bwd_kernel<T>;
+  constexpr size_t bytes = micro_smem<MICRO_PB>(4);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MICROB_SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((m.V + MICROB_P - 1) / MICROB_P), 1, 1);
-  cfg.blockDim = dim3(MICROB_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = MICROB_SMEM;
+  cfg.gridDim = dim3((unsigned)((m.V + MICRO_PB - 1) / MICRO_PB), 1, 1);
+  cfg.blockDim = dim3(MICRO_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
