@@ -735,8 +735,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       const int64_t base = fwd ? d.off_base : d.toff_base, nodes = fwd ? d.W : d.Wprev;
       int maxfan = 0;
       for (int64_t i = 0; i < nodes; ++i) maxfan = std::max(maxfan, o[base + i + 1] - o[base + i]);
-      if (d.W > MICRO_W || d.Wprev > MICRO_W || maxfan > MICRO_FAN || nodes + 1 + d.E > MICRO_CSR)
-        break;
+      const int wmax = fwd ? MICRO_WF : MICRO_WB, cmax = fwd ? MICRO_CSRF : MICRO_CSRB;
+      if (d.W > wmax || d.Wprev > wmax || maxfan > MICRO_FAN || nodes + 1 + d.E > cmax) break;
       --mf;
     }
     for (int32_t l = mf; l < num_layers; ++l) {

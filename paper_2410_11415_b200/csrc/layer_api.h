@@ -68,15 +68,17 @@ struct TailArgs {
   unsigned long long* trace_ts;  // KLAY_TAIL_TRACE=1: per-layer globaltimer stamps (debug)
 };
 
-// The micro tails: the thin top layers (every width <= MICRO_W, fan-in /
-// fan-out <= MICRO_FAN, one layer's CSR <= MICRO_CSR ints) evaluated by one
+// The micro tails: the thin top layers (widths <= MICRO_WF / MICRO_WB, fan-in
+// / fan-out <= MICRO_FAN, one layer's CSR <= MICRO_CSRF / MICRO_CSRB ints) evaluated by one
 // CTA per column chunk with the layer values held in shared memory. Each
 // layer's CSR (offsets local from 0, then indices) is packed at a 16-byte
 // aligned offset of one plan int array and staged per layer.
 constexpr int MICRO_MAX_LAYERS = 64;
-constexpr int MICRO_W = 1280;
+constexpr int MICRO_WF = 2560;   // forward: two row sets of 32-byte chunks
+constexpr int MICRO_WB = 1280;   // backward: four row sets of 32-byte chunks
 constexpr int MICRO_FAN = 129;
-constexpr int MICRO_CSR = 4096;  // ints
+constexpr int MICRO_CSRF = 8192;  // ints per staged layer CSR
+constexpr int MICRO_CSRB = 4096;
 template <typename T>
 struct MicroArgs {
   const T* in;                    // rows of the layer below the first micro layer

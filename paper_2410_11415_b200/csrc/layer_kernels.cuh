@@ -989,12 +989,10 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
 // sequential products / max / min, the streaming logsumexp of LseOp.
 
 constexpr int MICRO_THREADS = 512;
-constexpr int MICRO_PF = 4;  // forward: 64-byte column chunks
-constexpr int MICRO_PB = 2;  // backward: 32-byte column chunks (four row sets)
-template <int P>
-constexpr size_t micro_smem(int sets) {
-  return (size_t)sets * MICRO_W * P * 16 + (size_t)2 * MICRO_CSR * sizeof(int);
-}
+constexpr int MICRO_PF = 2;  // 32-byte column chunks
+constexpr int MICRO_PB = 2;
+constexpr size_t MICRO_SMEM_F = (size_t)2 * MICRO_WF * MICRO_PF * 16 + (size_t)2 * MICRO_CSRF * sizeof(int);
+constexpr size_t MICRO_SMEM_B = (size_t)4 * MICRO_WB * MICRO_PB * 16 + (size_t)2 * MICRO_CSRB * sizeof(int);
 
 template <typename T>
 __device__ __forceinline__ Vec<T> lds1(const uint4* p) {
@@ -1068,8 +1066,8 @@ template <typename T, int RKP, int RKS>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_kernel(const __grid_constant__ MicroArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
-  constexpr int P = MICRO_PF, NW = MICRO_THREADS / P;
-  constexpr size_t SET = (size_t)MICRO_W * P;
+  constexpr int P = MICRO_PF, NW = MICRO_THREADS / P, CSR = MICRO_CSRF;
+  constexpr size_t SET = (size_t)MICRO_WF * P;
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* rows = reinterpret_cast<uint4*>(smem);
   int* csr = reinterpret_cast<int*>(smem + 2 * SET * 16);
@@ -1090,12 +1088,12 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
   __syncthreads();
   for (int i = 0; i < m.n; ++i) {
     if (i + 1 < m.n) {
-      micro_stage_csr(csr + ((i + 1) & 1) * MICRO_CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
+      micro_stage_csr(csr + ((i + 1) & 1) * CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
       cp_async_commit();
     }
     const uint4* src = rows + (i & 1) * SET + hl;
     uint4* dst = rows + ((i + 1) & 1) * SET;
-    const int* off = csr + (i & 1) * MICRO_CSR;
+    const int* off = csr + (i & 1) * CSR;
     const int* idx = off + m.w[i] + 1;
     T* out = m.out[i];
     const bool prod = m.prod[i] != 0;
@@ -1114,7 +1112,7 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
 template <typename T, int RKP, int RKS>
 inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   auto kern = micro_kernel<T, RKP, RKS>;
-  constexpr size_t bytes = micro_smem<MICRO_PF>(2);
+  constexpr size_t bytes = MICRO_SMEM_F;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1137,8 +1135,8 @@ template <typename T>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_bwd_kernel(const __grid_constant__ MicroBwdArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
-  constexpr int P = MICRO_PB, NW = MICRO_THREADS / P;
-  constexpr size_t SET = (size_t)MICRO_W * P;
+  constexpr int P = MICRO_PB, NW = MICRO_THREADS / P, CSR = MICRO_CSRB;
+  constexpr size_t SET = (size_t)MICRO_WB * P;
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* gset = reinterpret_cast<uint4*>(smem);              // [2] adjoint row sets
   uint4* vp = reinterpret_cast<uint4*>(smem) + 2 * SET;      // parent values
@@ -1168,14 +1166,14 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
   for (int i = 0; i < m.n; ++i) {
     const bool logsum = m.logsum[i] != 0;
     if (i + 1 < m.n) {
-      micro_stage_csr(csr + ((i + 1) & 1) * MICRO_CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
+      micro_stage_csr(csr + ((i + 1) & 1) * CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
       // a product layer leaves vp / vx free for the log-sum layer below
       if (!logsum && m.logsum[i + 1]) fetch_values(i + 1);
       cp_async_commit();
     }
     const uint4* src = gset + (i & 1) * SET + hl;
     uint4* dst = gset + ((i + 1) & 1) * SET;
-    const int* off = csr + (i & 1) * MICRO_CSR;
+    const int* off = csr + (i & 1) * CSR;
     const int* idx = off + m.wc[i] + 1;
     T* out = m.gout[i];
     for (int c = worker; c < m.wc[i]; c += NW) {
@@ -1202,7 +1200,7 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
 template <typename T>
 inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
   auto kern = micro_bwd_kernel<T>;
-  constexpr size_t bytes = micro_smem<MICRO_PB>(4);
+  constexpr size_t bytes = MICRO_SMEM_B;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
