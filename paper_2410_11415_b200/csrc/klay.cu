@@ -95,6 +95,17 @@ const int g_chunk_order = [] {
   const char* e = getenv("KLAY_CHUNK_ORDER");
   return (e && *e) ? atoi(e) : 1;
 }();
+// The micro tails run one CTA (of ~200 KB shared memory) per 32-byte column
+// chunk; beyond two waves of them (very large batches) the layer kernels,
+// which spread each layer over the whole GPU, are used instead.
+bool micro_fits(int V) {
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return (V + MICRO_P - 1) / MICRO_P <= 2 * sms;
+}
 int chunk_rev(int l) { return g_chunk_order == 1 ? (l & 1) : g_chunk_order == 2 ? ((l >> 1) & 1) : 0; }
 
 // KLAY_NO_ALIAS=1: every sum row is computed and read (A/B switch)
@@ -903,7 +914,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     KLAY_CUDA(cudaMemsetAsync(hcount, 0, counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld), s));
   }
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
-  const int32_t micro_from = (g_no_tail || g_no_micro) ? p->L : p->micro_from;
+  const int32_t micro_from = (g_no_tail || g_no_micro || !micro_fits(V)) ? p->L : p->micro_from;
   TailArgs<T>* tail = nullptr;
   if (tail_from < micro_from) {
     tail = new TailArgs<T>();
@@ -1046,7 +1057,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
   // the backward micro tail covers the log semiring (pass / log-sum layers)
   const int32_t microb_from =
-      (g_no_tail || g_no_micro || domain != SR_LOG_) ? p->L : p->microb_from;
+      (g_no_tail || g_no_micro || domain != SR_LOG_ || !micro_fits(V)) ? p->L : p->microb_from;
   MicroBwdArgs<T> mb{};
   TailArgs<T>* tail = nullptr;
   if (tail_from < microb_from) {

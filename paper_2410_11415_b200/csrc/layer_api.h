@@ -74,6 +74,7 @@ struct TailArgs {
 // layer's CSR (offsets local from 0, then indices) is packed at a 16-byte
 // aligned offset of one plan int array and staged per layer.
 constexpr int MICRO_MAX_LAYERS = 64;
+constexpr int MICRO_P = 2;        // 16-byte pieces per CTA column chunk (32 bytes)
 constexpr int MICRO_WF = 2560;   // forward: two row sets of 32-byte chunks
 constexpr int MICRO_WB = 1280;   // backward: four row sets of 32-byte chunks
 constexpr int MICRO_FAN = 129;

@@ -989,8 +989,8 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
 // sequential products / max / min, the streaming logsumexp of LseOp.
 
 constexpr int MICRO_THREADS = 512;
-constexpr int MICRO_PF = 2;  // 32-byte column chunks
-constexpr int MICRO_PB = 2;
+constexpr int MICRO_PF = MICRO_P;
+constexpr int MICRO_PB = MICRO_P;
 constexpr size_t MICRO_SMEM_F = (size_t)2 * MICRO_WF * MICRO_PF * 16 + (size_t)2 * MICRO_CSRF * sizeof(int);
 constexpr size_t MICRO_SMEM_B = (size_t)4 * MICRO_WB * MICRO_PB * 16 + (size_t)2 * MICRO_CSRB * sizeof(int);
 
