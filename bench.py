@@ -63,11 +63,36 @@ def _tail_from(tc):
     return t
 
 
+def _micro_from(tc, fwd):
+    """First layer of libklay's forward / backward micro tail (klay.cu
+    micro_suffix: longest suffix of <= 64 layers with widths <= 2560 / 1280,
+    fan-in / fan-out <= 129 and one layer's CSR <= 8192 / 4096 ints)."""
+    wmax, cmax = (2560, 8192) if fwd else (1280, 4096)
+    L = len(tc.layers)
+    widths = [tc.num_inputs] + [l.width for l in tc.layers]
+    m = L
+    while m > 0 and L - m < 64:
+        layer = tc.layers[m - 1]
+        W, Wp, E = widths[m], widths[m - 1], len(layer.sources)
+        key = layer.segments if fwd else layer.sources
+        fan = int(np.bincount(np.asarray(key), minlength=W if fwd else Wp).max())
+        nodes = W if fwd else Wp
+        if W > wmax or Wp > wmax or fan > 129 or nodes + 1 + E > cmax:
+            break
+        m -= 1
+    return m
+
+
+def _alias_bound(tc):
+    """Nodes of layers >= this bound are never aliased (read by a tail)."""
+    return min(_tail_from(tc), _micro_from(tc, True), _micro_from(tc, False))
+
+
 _ALIAS_PLANS = {}
 
 
 def alias_plan(tc):
-    key = (id(tc), _tail_from(tc))
+    key = (id(tc), _alias_bound(tc))
     if key not in _ALIAS_PLANS:
         _ALIAS_PLANS[key] = _alias_plan(tc)
     return _ALIAS_PLANS[key]
@@ -78,7 +103,7 @@ def _alias_plan(tc):
     (klay.cu build_aliases), for the byte model: per node layer, which nodes
     are aliased, their source row, and which adjoints are routed."""
     L = len(tc.layers)
-    tail = _tail_from(tc)
+    tail = _alias_bound(tc)
     widths = [tc.num_inputs] + [l.width for l in tc.layers]
     rows = np.cumsum([0] + widths)
     child, npar, par, ali, srow = [], [], [], [], []

@@ -31,6 +31,7 @@ SIGNATURES = {
     "klay_plan_destroy": (ctypes.c_int, [_vp]),
     "klay_plan_num_nodes": (_c_i64, [_vp]),
     "klay_plan_max_width": (_c_i64, [_vp]),
+    "klay_plan_schedule": (ctypes.c_int, [_vp, _vp]),
     "klay_plan_layer_offset": (_c_i64, [_vp, _c_i32]),
     "klay_row_stride": (_c_i64, [_c_i64, _c_i32]),
     "klay_forward": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _c_i32, _vp, _c_i64, _c_i32, _vp,

@@ -822,6 +822,15 @@ extern "C" int klay_plan_destroy(KlayPlan* plan) {
 
 extern "C" int64_t klay_plan_num_nodes(const KlayPlan* p) { return p ? p->total_rows : -1; }
 extern "C" int64_t klay_plan_max_width(const KlayPlan* p) { return p ? p->max_width : -1; }
+
+extern "C" int klay_plan_schedule(const KlayPlan* p, int64_t* out) {
+  if (!p || !out) return fail(KLAY_EINVAL, "klay_plan_schedule: null argument");
+  out[0] = p->tail_from;
+  out[1] = p->micro_from;
+  out[2] = p->microb_from;
+  out[3] = p->n_alias;
+  return KLAY_OK;
+}
 extern "C" int64_t klay_plan_layer_offset(const KlayPlan* p, int32_t l) {
   if (!p || l < 0 || l > p->L) return -1;
   return p->layer_row[l];

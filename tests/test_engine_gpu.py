@@ -463,3 +463,21 @@ def test_alias_and_tail_extremes(cuda, tail_edges, no_micro):
          "-k", "golden_small or nonfinite or backward_only or consumer or random_circuits"],
         env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("cfg", ["B", "C", "D", "E"])
+def test_plan_schedule_matches_byte_model(cuda, cfg):
+    """bench.py's byte model restates the plan builder's schedule (tail and
+    micro-tail boundaries) and its unary-node aliases; both must agree with
+    the library's own plan (klay_plan_schedule)."""
+    import bench
+    from paper_2410_11415_b200 import device_plan
+    tc, _ = load_config(cfg)
+    plan = device_plan(tc)
+    s = plan.schedule
+    assert s["tail"] == bench._tail_from(tc)
+    assert s["micro"] == bench._micro_from(tc, True)
+    assert s["micro_bwd"] == bench._micro_from(tc, False)
+    ap = bench.alias_plan(tc)
+    n_alias = sum(int(np.asarray(a).sum()) for a in ap["ali"]) if ap is not None else 0
+    assert s["aliased_rows"] == n_alias
