@@ -124,3 +124,59 @@ def test_random_wide_circuits_all_semirings(cuda, seed):
     ref, _ = oracle.forward(tc, w, "maxprod", retain=False)
     got = engine.evaluate_semiring(tc, engine.WeightAssignment(w), "maxprod")
     assert np.array_equal(got, ref)
+
+
+def fanin_circuit(seed, K=64, L=8, W=48, fmax=110):
+    """Every sum node draws its fan-in from 1..fmax, every product node from
+    1..3 (children with repetition allowed, each previous node read at least
+    once; values stay finite): numpy's 8-accumulator pairwise order inside
+    the micro tails (fan-in and fan-out 9..129)."""
+    from paper_2410_11415_b200.tensorized import Literal, TensorizedCircuit, TensorLayer, validate
+    rng = np.random.default_rng(seed)
+    layers, prev = [], K
+    for l in range(L):
+        w = W if l < L - 1 else 2
+        f = 3 if l % 2 == 0 else fmax
+        segs = [rng.integers(0, prev, size=int(rng.integers(1, f + 1))).tolist() for _ in range(w)]
+        for c in range(prev):  # every child read
+            segs[int(rng.integers(0, w))].append(c)
+        src = np.array([c for s in segs for c in s], np.int64)
+        seg = np.array([p for p, s in enumerate(segs) for _ in s], np.int64)
+        layers.append(TensorLayer("prod" if l % 2 == 0 else "sum", w, src, seg))
+        prev = w
+    input_map = {Literal(v, pos): 2 * (v - 1) + (0 if pos else 1)
+                 for v in range(1, K // 2 + 1) for pos in (True, False)}
+    tc = TensorizedCircuit(K, K // 2, layers, input_map, [0, 1], {})
+    validate(tc)
+    return tc
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_micro_tail_pairwise_fanin(cuda, seed):
+    """Fan-ins and fan-outs up to 129 inside the micro tails: real fp64
+    values and gradients bit-exact (x0 + numpy pairwise of the rest), log
+    fp64 within 1e-12."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan
+    tc = fanin_circuit(300 + seed)
+    assert max(np.bincount(l.segments).max() for l in tc.layers) > 64
+    assert max(np.bincount(l.sources).max() for l in tc.layers) > 32
+    plan = device_plan(tc)
+    assert plan.schedule["micro"] == 0 and plan.schedule["micro_bwd"] == 0
+    rng = np.random.default_rng(seed)
+    B = (1, 7, 64)[seed % 3]
+    w = rng.uniform(0.05, 0.15, size=(B, tc.num_inputs)) * rng.choice([-1.0, 1.0], size=(B, tc.num_inputs))
+    x = torch.tensor(w, dtype=torch.float64, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_REAL, np.float64)
+    g = plan.backward(vals, B, _lib.KLAY_REAL, np.float64)
+    ref, tr = oracle.forward(tc, w, "real")
+    assert np.array_equal(out.cpu().numpy(), ref, equal_nan=True)
+    np.testing.assert_array_equal(g.cpu().numpy(), oracle.backward(tc, tr, "real"))
+    lw = np.log(np.abs(w))
+    x = torch.tensor(lw, dtype=torch.float64, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_LOG, np.float64)
+    g = plan.backward(vals, B, _lib.KLAY_LOG, np.float64)
+    ref, tr = oracle.forward(tc, lw, "log")
+    rel_close(out.cpu().numpy(), ref, 1e-12, 1e-12)
+    rel_close(g.cpu().numpy(), oracle.backward(tc, tr, "log"), 1e-12, 1e-12)
