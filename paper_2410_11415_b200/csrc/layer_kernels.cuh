@@ -9,6 +9,8 @@
 // which stays L2-resident while its rows are gathered ~2.7 times each.
 #pragma once
 
+#include <atomic>
+
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -680,6 +682,15 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
 }
 
 // KLAY_NO_PDL=1 launches layer kernels fully serialized (A/B switch)
+// Kernel attributes (shared-memory opt-in, carveout, cluster size) are set
+// once per kernel and device: `mask` holds one bit per configured device.
+inline bool needs_config(std::atomic<unsigned>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  return !(mask.fetch_or(bit) & bit);
+}
+
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("KLAY_NO_PDL");
@@ -768,8 +779,8 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
   if (a.n_items > 0) {
     ++launched;
     constexpr size_t smem = ItemsSmem<T, G>::bytes;
-    static bool configured = false;  // opt in to > 48 KB dynamic smem once per kernel
-    if (!configured) {
+    static std::atomic<unsigned> configured{0};  // opt in to > 48 KB dynamic smem
+    if (needs_config(configured)) {
       cudaFuncSetAttribute(items_kernel<T, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       // one carveout for every layer kernel: consecutive launches never wait
@@ -778,7 +789,6 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
                            cudaSharedmemCarveoutMaxShared);
       cudaFuncSetAttribute(combine_kernel<T, RK, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
-      configured = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
@@ -795,12 +805,10 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
   if (a.n_heavy > 0 && !a.hcount) {
     ++launched;
     constexpr size_t csmem = (size_t)COMBINE_LEAVES * 32 * NV * 16;
-    static bool cconf = false;
-    if (!cconf) {
+    static std::atomic<unsigned> cconf{0};
+    if (needs_config(cconf))
       cudaFuncSetAttribute(combine_kernel<T, RK, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)csmem);
-      cconf = true;
-    }
     dim3 grid((unsigned)a.n_heavy, chunks);
     combine_kernel<T, RK, G><<<grid, 32, csmem, s>>>(a);
   }
@@ -941,13 +949,12 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
   const int chunks = (t.layer[0].V + 32 * NV - 1) / (32 * NV);
   auto kern = tail_kernel<T, RKP, RKS, GP, GS>;
   constexpr size_t smem = TailSmem<T, GP, GS>::bytes;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned> configured{0};
+  if (needs_config(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(chunks * cluster), 1, 1);
@@ -1113,10 +1120,9 @@ template <typename T, int RKP, int RKS>
 inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   auto kern = micro_kernel<T, RKP, RKS>;
   constexpr size_t bytes = MICRO_SMEM_F;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned> configured{0};
+  if (needs_config(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((m.V + MICRO_PF - 1) / MICRO_PF), 1, 1);
@@ -1201,10 +1207,9 @@ template <typename T>
 inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
   auto kern = micro_bwd_kernel<T>;
   constexpr size_t bytes = MICRO_SMEM_B;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned> configured{0};
+  if (needs_config(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((m.V + MICRO_PB - 1) / MICRO_PB), 1, 1);
