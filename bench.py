@@ -66,8 +66,8 @@ def _tail_from(tc):
 def _micro_from(tc, fwd):
     """First layer of libklay's forward / backward micro tail (klay.cu
     micro_suffix: longest suffix of <= 64 layers with widths <= 2560 / 1280,
-    fan-in / fan-out <= 129 and one layer's CSR <= 8192 / 4096 ints)."""
-    wmax, cmax = (2560, 8192) if fwd else (1280, 4096)
+    fan-in / fan-out <= 129 and one layer's CSR <= 8192 ints; log semiring)."""
+    wmax, cmax = (2560, 8192) if fwd else (1280, 8192)
     L = len(tc.layers)
     widths = [tc.num_inputs] + [l.width for l in tc.layers]
     m = L
@@ -632,6 +632,7 @@ def run_gpu_arm(args):
         extra = {
             "A_real_f64_b1_fwd": measure_config("A", "real", np.float64, 1, False, dev),
             "B_log_f64_b256_fwd_bwd": measure_config("B", "log", np.float64, 256, True, dev),
+            "B_real_f64_b256_fwd_bwd": measure_config("B", "real", np.float64, 256, True, dev),
             "D_bool_b4096_fwd": measure_config("D", "bool", np.float32, 4096, False, dev),
             "D_bool_packed_b4096_fwd": measure_config("D", "bool_packed", "u1", 4096, False, dev),
             "D_real_f32_b4096_fwd": measure_config("D", "real", np.float32, 4096, False, dev),

@@ -20,8 +20,9 @@ int launch_backward_tail(int domain, const TailArgs<float>& t, int cluster, cuda
   return launch_tail<float, RK_SUM, RK_SUM, BwdGather<float, BW_REALPROD>, PASS>(t, cluster, s);
 }
 
-int launch_backward_micro(const MicroBwdArgs<float>& m, cudaStream_t s) {
-  return launch_micro_bwd<float>(m, s);
+int launch_backward_micro(int domain, const MicroBwdArgs<float>& m, cudaStream_t s) {
+  if (domain == SR_LOG) return launch_micro_bwd<float, SR_LOG>(m, s);
+  return launch_micro_bwd<float, SR_REAL>(m, s);
 }
 
 }  // namespace klay

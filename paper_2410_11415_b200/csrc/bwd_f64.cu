@@ -20,8 +20,9 @@ int launch_backward_tail(int domain, const TailArgs<double>& t, int cluster, cud
   return launch_tail<double, RK_SUM, RK_SUM, BwdGather<double, BW_REALPROD>, PASS>(t, cluster, s);
 }
 
-int launch_backward_micro(const MicroBwdArgs<double>& m, cudaStream_t s) {
-  return launch_micro_bwd<double>(m, s);
+int launch_backward_micro(int domain, const MicroBwdArgs<double>& m, cudaStream_t s) {
+  if (domain == SR_LOG) return launch_micro_bwd<double, SR_LOG>(m, s);
+  return launch_micro_bwd<double, SR_REAL>(m, s);
 }
 
 }  // namespace klay

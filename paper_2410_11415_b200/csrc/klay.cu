@@ -342,8 +342,10 @@ struct KlayPlan {
   int32_t micro_from = 0;  // first layer of the forward micro tail (L = none)
   std::vector<int> micro_at, micro_n;  // per micro layer: offset / length of its CSR in d_micro
   int* d_micro = nullptr;  // packed micro-tail CSR ([W+1] local offsets, [E] indices per layer)
-  int32_t microb_from = 0;  // first layer of the backward micro tail (L = none)
-  std::vector<int> microb_at, microb_n;  // per layer from microb_from: its transposed CSR
+  int32_t microb_from = 0;  // first layer of the backward micro tail, log semiring (L = none)
+  int32_t microb_from_real = 0;  // ... real semiring (>= microb_from)
+  std::vector<int> microb_at, microb_n, microbr_n;  // per layer from microb_from: its CSR
+                                                   // block, staged length (log / real)
   int* d_microb = nullptr;
 };
 
@@ -737,37 +739,52 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   // micro tails: the longest suffix of layers that fit them (widths, fan-in
   // (forward) / fan-out (backward) and one layer's CSR bounded); a layer's
   // CSR block starts 16-byte aligned for the per-layer cp.async staging
-  auto micro_suffix = [&](bool fwd, std::vector<int>& packed, std::vector<int>& at,
-                          std::vector<int>& len) -> int32_t {
+  // mode 0: forward; 1: backward, log semiring (transposed CSR); 2: backward,
+  // real semiring (product layers also need their forward CSR: zero-safe
+  // adjoint). Returns the first layer of the longest qualifying suffix.
+  auto micro_suffix = [&](int mode) -> int32_t {
     int32_t mf = num_layers;
     while (mf > 0 && num_layers - mf < MICRO_MAX_LAYERS) {
       const LayerDesc& d = p->layers[mf - 1];
+      const bool fwd = mode == 0;
       const std::vector<int>& o = fwd ? off : toff;
       const int64_t base = fwd ? d.off_base : d.toff_base, nodes = fwd ? d.W : d.Wprev;
       int maxfan = 0;
       for (int64_t i = 0; i < nodes; ++i) maxfan = std::max(maxfan, o[base + i + 1] - o[base + i]);
       const int wmax = fwd ? MICRO_WF : MICRO_WB, cmax = fwd ? MICRO_CSRF : MICRO_CSRB;
-      if (d.W > wmax || d.Wprev > wmax || maxfan > MICRO_FAN || nodes + 1 + d.E > cmax) break;
+      const int64_t ints = nodes + 1 + d.E + ((mode == 2 && d.prod) ? d.W + 1 + d.E : 0);
+      if (d.W > wmax || d.Wprev > wmax || maxfan > MICRO_FAN || ints > cmax) break;
       --mf;
-    }
-    for (int32_t l = mf; l < num_layers; ++l) {
-      const LayerDesc& d = p->layers[l];
-      at.push_back((int)packed.size());
-      if (fwd) {
-        for (int64_t i = 0; i <= d.W; ++i) packed.push_back(off[d.off_base + i]);
-        for (int64_t e = 0; e < d.E; ++e) packed.push_back(src[d.e_base + e]);
-      } else {
-        for (int64_t j = 0; j <= d.Wprev; ++j) packed.push_back(toff[d.toff_base + j]);
-        for (int64_t e = 0; e < d.E; ++e) packed.push_back(tpar[d.e_base + e]);
-      }
-      len.push_back((int)packed.size() - at.back());
-      while (packed.size() % 4) packed.push_back(0);
     }
     return mf;
   };
   std::vector<int> micro, microb;
-  p->micro_from = micro_suffix(true, micro, p->micro_at, p->micro_n);
-  p->microb_from = micro_suffix(false, microb, p->microb_at, p->microb_n);
+  p->micro_from = micro_suffix(0);
+  p->microb_from = micro_suffix(1);
+  p->microb_from_real = std::max(micro_suffix(2), p->microb_from);
+  for (int32_t l = p->micro_from; l < num_layers; ++l) {
+    const LayerDesc& d = p->layers[l];
+    p->micro_at.push_back((int)micro.size());
+    for (int64_t i = 0; i <= d.W; ++i) micro.push_back(off[d.off_base + i]);
+    for (int64_t e = 0; e < d.E; ++e) micro.push_back(src[d.e_base + e]);
+    p->micro_n.push_back((int)micro.size() - p->micro_at.back());
+    while (micro.size() % 4) micro.push_back(0);
+  }
+  // backward blocks: [transposed offsets, parents], then for product layers
+  // [forward offsets, children] (staged by the real semiring only)
+  for (int32_t l = p->microb_from; l < num_layers; ++l) {
+    const LayerDesc& d = p->layers[l];
+    p->microb_at.push_back((int)microb.size());
+    for (int64_t j = 0; j <= d.Wprev; ++j) microb.push_back(toff[d.toff_base + j]);
+    for (int64_t e = 0; e < d.E; ++e) microb.push_back(tpar[d.e_base + e]);
+    p->microb_n.push_back((int)microb.size() - p->microb_at.back());
+    if (d.prod) {
+      for (int64_t i = 0; i <= d.W; ++i) microb.push_back(off[d.off_base + i]);
+      for (int64_t e = 0; e < d.E; ++e) microb.push_back(src[d.e_base + e]);
+    }
+    p->microbr_n.push_back((int)microb.size() - p->microb_at.back());
+    while (microb.size() % 4) microb.push_back(0);
+  }
   if (num_layers >= 2 && row < (1LL << 30)) {
     build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
                   alias_rows,
@@ -1065,8 +1082,8 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   const bool alias = domain == SR_LOG_ && epsilon == 0.0 && retain_mode == 2 && !g_no_alias;
   const int32_t tail_from = g_no_tail ? p->L : p->tail_from;
   // the backward micro tail covers the log semiring (pass / log-sum layers)
-  const int32_t microb_from =
-      (g_no_tail || g_no_micro || domain != SR_LOG_ || !micro_fits(V)) ? p->L : p->microb_from;
+  const int32_t microb_from = (g_no_tail || g_no_micro || !micro_fits(V)) ? p->L
+                               : (domain == SR_LOG_ ? p->microb_from : p->microb_from_real);
   MicroBwdArgs<T> mb{};
   TailArgs<T>* tail = nullptr;
   if (tail_from < microb_from) {
@@ -1099,15 +1116,16 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       mb.wp[i] = (int)d.W;
       mb.wc[i] = (int)d.Wprev;
       mb.csr_at[i] = p->microb_at[l - p->microb_from];
-      mb.csr_n[i] = p->microb_n[l - p->microb_from];
-      mb.logsum[i] = d.prod ? 0 : 1;
+      mb.csr_n[i] = (domain == SR_LOG_ ? p->microb_n : p->microbr_n)[l - p->microb_from];
+      // weighted layers: log sums (softmax weights), real products (zero-safe)
+      mb.logsum[i] = (domain == SR_LOG_) ? (d.prod ? 0 : 1) : (d.prod ? 1 : 0);
       if (l == microb_from) {
         mb.csr = p->d_microb;
         mb.V = V;
         mb.ld = ld;
         mb.unary_ok = a.unary_ok;
         LaunchScope ls(s, 7, microb_from + 1);
-        const int n = launch_backward_micro(mb, s);
+        const int n = launch_backward_micro(domain, mb, s);
         if (n == 0) return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
                                                 cudaGetErrorString(cudaGetLastError()));
         g_launches += n;

@@ -79,7 +79,7 @@ constexpr int MICRO_WF = 2560;   // forward: two row sets of 32-byte chunks
 constexpr int MICRO_WB = 1280;   // backward: four row sets of 32-byte chunks
 constexpr int MICRO_FAN = 129;
 constexpr int MICRO_CSRF = 8192;  // ints per staged layer CSR
-constexpr int MICRO_CSRB = 4096;
+constexpr int MICRO_CSRB = 8192;
 template <typename T>
 struct MicroArgs {
   const T* in;                    // rows of the layer below the first micro layer
@@ -93,8 +93,8 @@ struct MicroArgs {
   long long ld;
   T eps;
 };
-// backward micro tail (log semiring): steps i = 0.. walk the micro layers top
-// down; step i computes the children's adjoints of one layer
+// backward micro tail: steps i = 0.. walk the micro layers top down; step i
+// computes the children's adjoints of one layer
 template <typename T>
 struct MicroBwdArgs {
   const T* gin;                     // adjoint rows of the top layer (seeded)
@@ -105,13 +105,13 @@ struct MicroBwdArgs {
   int wc[MICRO_MAX_LAYERS];
   int csr_at[MICRO_MAX_LAYERS];     // [wc+1 transposed offsets, E parent indices] in csr
   int csr_n[MICRO_MAX_LAYERS];
-  int logsum[MICRO_MAX_LAYERS];     // sum layer (weighted edges) / product layer (pass)
+  int logsum[MICRO_MAX_LAYERS];     // weighted edges (log sum / real product) or pass-through
   const int* csr;
   int n, w_top, V, unary_ok;
   long long ld;
 };
-int launch_backward_micro(const MicroBwdArgs<float>& m, cudaStream_t s);
-int launch_backward_micro(const MicroBwdArgs<double>& m, cudaStream_t s);
+int launch_backward_micro(int domain, const MicroBwdArgs<float>& m, cudaStream_t s);
+int launch_backward_micro(int domain, const MicroBwdArgs<double>& m, cudaStream_t s);
 int launch_forward_micro(int sr, const MicroArgs<float>& m, cudaStream_t s);
 int launch_forward_micro(int sr, const MicroArgs<double>& m, cudaStream_t s);
 int launch_forward_micro_u1(const MicroArgs<unsigned>& m, cudaStream_t s);

@@ -985,11 +985,12 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
 // the current layer runs.
 //
 // Forward (any semiring): two layers' value rows (ping-pong); each result
-// goes to shared memory and to the trace. Backward (log semiring): two
-// layers' adjoint rows plus, for a log-sum layer, the forward values of its
-// parents and children, fetched with cp.async while the product layer above
-// it runs (layers alternate product / sum). Only the lowest layer's adjoints
-// leave the CTA.
+// goes to shared memory and to the trace. Backward: two layers' adjoint rows
+// plus, for a weighted layer (log: sums, softmax weights; real: products,
+// zero-safe adjoint over the layer's forward CSR), the forward values of its
+// parents and children, fetched with cp.async while the pass-through layer
+// above it runs (layers alternate product / sum). Only the lowest layer's
+// adjoints leave the CTA.
 //
 // Reductions follow the reference's order exactly: x0 + numpy's pairwise sum
 // of the rest (fan-in <= MICRO_FAN = PW_BLOCK + 1: one pairwise block),
@@ -1137,7 +1138,7 @@ inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, m) == cudaSuccess ? 1 : 0;
 }
 
-template <typename T>
+template <typename T, int DOM>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_bwd_kernel(const __grid_constant__ MicroBwdArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
@@ -1170,29 +1171,66 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
   cp_async_wait<0>();
   __syncthreads();
   for (int i = 0; i < m.n; ++i) {
-    const bool logsum = m.logsum[i] != 0;
+    const bool weighted = m.logsum[i] != 0;
     if (i + 1 < m.n) {
       micro_stage_csr(csr + ((i + 1) & 1) * CSR, m.csr + m.csr_at[i + 1], m.csr_n[i + 1]);
-      // a product layer leaves vp / vx free for the log-sum layer below
-      if (!logsum && m.logsum[i + 1]) fetch_values(i + 1);
+      // a pass-through layer leaves vp / vx free for the weighted layer below
+      if (!weighted && m.logsum[i + 1]) fetch_values(i + 1);
       cp_async_commit();
     }
     const uint4* src = gset + (i & 1) * SET + hl;
     uint4* dst = gset + ((i + 1) & 1) * SET;
     const int* off = csr + (i & 1) * CSR;
     const int* idx = off + m.wc[i] + 1;
+    // real products: the layer's forward CSR follows (zero-safe adjoint)
+    const int* foff = idx + off[m.wc[i]];
+    const int* fsrc = foff + m.wp[i] + 1;
     T* out = m.gout[i];
     for (int c = worker; c < m.wc[i]; c += NW) {
       const int e0 = off[c], n = off[c + 1] - e0;
       Vec<T> x{};
-      if (logsum) x = lds1<T>(vx + c * P + hl);
+      if (weighted) x = lds1<T>(vx + c * P + hl);
       auto val = [&](int e) {
         const int row = idx[e0 + e];
         const int p = row & 0x7fffffff;
         const Vec<T> g = lds1<T>(src + (size_t)p * P);
-        if (!logsum) return g;
-        if (row < 0 && m.unary_ok) return BwdGather<T, BW_LOGSUM>::unary(g, x);
-        return BwdGather<T, BW_LOGSUM>::logsum_edge(g, lds1<T>(vp + (size_t)p * P + hl), x);
+        if (!weighted) return g;
+        if constexpr (DOM == SR_LOG) {
+          if (row < 0 && m.unary_ok) return BwdGather<T, BW_LOGSUM>::unary(g, x);
+          return BwdGather<T, BW_LOGSUM>::logsum_edge(g, lds1<T>(vp + (size_t)p * P + hl), x);
+        } else {
+          const Vec<T> pv = lds1<T>(vp + (size_t)p * P + hl);
+          // (g * prod) / x; a segment holding a zero (or a NaN product)
+          // counts its zeros (BwdGather<BW_REALPROD>::combine / zero_path)
+          constexpr int N = Vec<T>::N;
+          Vec<T> r;
+          bool any_zero = false;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            r.v[k] = (g.v[k] * pv.v[k]) / x.v[k];
+            any_zero |= (x.v[k] == T(0)) | (pv.v[k] == T(0)) | (pv.v[k] != pv.v[k]);
+          }
+          if (any_zero) {
+            T pnz[N];
+            int zc[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) { pnz[k] = T(1); zc[k] = 0; }
+            for (int q = foff[p]; q < foff[p + 1]; ++q) {
+              const Vec<T> y = lds1<T>(vx + (size_t)fsrc[q] * P + hl);
+#pragma unroll
+              for (int k = 0; k < N; ++k) {
+                if (y.v[k] == T(0)) ++zc[k];
+                else pnz[k] *= y.v[k];
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              if (x.v[k] == T(0)) r.v[k] = (zc[k] == 1) ? g.v[k] * pnz[k] : T(0);
+              else if (zc[k] > 0) r.v[k] = T(0);
+            }
+          }
+          return r;
+        }
       };
       const Vec<T> r = micro_sum<T>(n, val);
       sts1(dst + c * P + hl, r);
@@ -1203,9 +1241,9 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
   }
 }
 
-template <typename T>
+template <typename T, int DOM>
 inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
-  auto kern = micro_bwd_kernel<T>;
+  auto kern = micro_bwd_kernel<T, DOM>;
   constexpr size_t bytes = MICRO_SMEM_B;
   static std::atomic<unsigned> configured{0};
   if (needs_config(configured)) {
