@@ -63,22 +63,37 @@ def _tail_from(tc):
     return t
 
 
+def _micro_ok(tc, l, fwd):
+    widths = [tc.num_inputs] + [x.width for x in tc.layers]
+    wmax = 2560 if fwd else 1280
+    layer = tc.layers[l]
+    W, Wp, E = widths[l + 1], widths[l], len(layer.sources)
+    key = layer.segments if fwd else layer.sources
+    fan = int(np.bincount(np.asarray(key), minlength=W if fwd else Wp).max())
+    nodes = W if fwd else Wp
+    return W <= wmax and Wp <= wmax and fan <= 129 and nodes + 1 + E <= 8192
+
+
+def _micro_head(tc, fwd):
+    """Layers in libklay's forward / backward micro head (klay.cu micro_head:
+    the longest qualifying prefix of <= 256-node layers below every tail, at
+    least two layers)."""
+    lim = min(_micro_from(tc, fwd), _tail_from(tc))
+    h = 0
+    widths = [tc.num_inputs] + [x.width for x in tc.layers]
+    while (h < lim and h < 64 and _micro_ok(tc, h, fwd)
+           and widths[h + 1] <= 256 and widths[h] <= 256):
+        h += 1
+    return h if h >= 2 else 0
+
+
 def _micro_from(tc, fwd):
     """First layer of libklay's forward / backward micro tail (klay.cu
     micro_suffix: longest suffix of <= 64 layers with widths <= 2560 / 1280,
     fan-in / fan-out <= 129 and one layer's CSR <= 8192 ints; log semiring)."""
-    wmax, cmax = (2560, 8192) if fwd else (1280, 8192)
     L = len(tc.layers)
-    widths = [tc.num_inputs] + [l.width for l in tc.layers]
     m = L
-    while m > 0 and L - m < 64:
-        layer = tc.layers[m - 1]
-        W, Wp, E = widths[m], widths[m - 1], len(layer.sources)
-        key = layer.segments if fwd else layer.sources
-        fan = int(np.bincount(np.asarray(key), minlength=W if fwd else Wp).max())
-        nodes = W if fwd else Wp
-        if W > wmax or Wp > wmax or fan > 129 or nodes + 1 + E > cmax:
-            break
+    while m > 0 and L - m < 64 and _micro_ok(tc, m - 1, fwd):
         m -= 1
     return m
 
@@ -104,6 +119,8 @@ def _alias_plan(tc):
     are aliased, their source row, and which adjoints are routed."""
     L = len(tc.layers)
     tail = _alias_bound(tc)
+    hmax = max(_micro_head(tc, True), _micro_head(tc, False))
+    lo = hmax + 2 if hmax else 1
     widths = [tc.num_inputs] + [l.width for l in tc.layers]
     rows = np.cumsum([0] + widths)
     child, npar, par, ali, srow = [], [], [], [], []
@@ -122,7 +139,7 @@ def _alias_plan(tc):
         npar[l] += np.bincount(src, minlength=widths[l])
         par[l][src] = seg
     is_sum = lambda nl: nl >= 1 and (nl - 1) % 2 == 1
-    for nl in range(1, min(L, tail)):
+    for nl in range(lo, min(L, tail)):
         m = child[nl] >= 0
         ali[nl] = m
         srow[nl][m] = srow[nl - 1][child[nl][m]]

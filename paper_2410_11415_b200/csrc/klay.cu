@@ -115,6 +115,12 @@ const bool g_no_micro = [] {
   return e && *e && *e != '0';
 }();
 
+// KLAY_NO_HEAD=1: the thin bottom layers run as layer kernels (A/B switch)
+const bool g_no_head = [] {
+  const char* e = getenv("KLAY_NO_HEAD");
+  return e && *e && *e != '0';
+}();
+
 const bool g_no_alias = [] {
   const char* e = getenv("KLAY_NO_ALIAS");
   return e && *e && *e != '0';
@@ -340,12 +346,15 @@ struct KlayPlan {
   int64_t WL = 0;  // width of the last layer (K when there are no gates)
   int32_t tail_from = 0;  // first layer of the persistent tail (L = no tail)
   int32_t micro_from = 0;  // first layer of the forward micro tail (L = none)
-  std::vector<int> micro_at, micro_n;  // per micro layer: offset / length of its CSR in d_micro
+  std::vector<int> micro_at, micro_n;  // per layer: offset / length of its CSR in d_micro (-1: none)
   int* d_micro = nullptr;  // packed micro-tail CSR ([W+1] local offsets, [E] indices per layer)
   int32_t microb_from = 0;  // first layer of the backward micro tail, log semiring (L = none)
   int32_t microb_from_real = 0;  // ... real semiring (>= microb_from)
-  std::vector<int> microb_at, microb_n, microbr_n;  // per layer from microb_from: its CSR
-                                                   // block, staged length (log / real)
+  std::vector<int> microb_at, microb_n, microbr_n;  // per layer: its CSR block, staged
+                                                   // length (log / real); -1: none
+  // micro heads: the thin bottom layers [0, head) in one launch per direction
+  // (0 = none); no node of layers <= max head + 1 is aliased
+  int32_t head_f = 0, head_b = 0, head_b_real = 0;
   int* d_microb = nullptr;
 };
 
@@ -408,6 +417,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
   const int L = p->L;
   // nodes read by a tail (persistent or micro) are never aliased
   const int tail = std::min({p->tail_from, p->micro_from, p->microb_from});
+  const int hmax = std::max({p->head_f, p->head_b, p->head_b_real});
+  const int lo = hmax > 0 ? hmax + 2 : 1;
   auto width = [&](int nl) -> int64_t { return nl == 0 ? K : widths[nl - 1]; };
   auto is_sum = [](int nl) { return nl >= 1 && ((nl - 1) % 2 == 1); };
   std::vector<std::vector<int>> child(L + 1), npar(L + 1), par(L + 1), up(L + 1), srow(L + 1),
@@ -441,7 +452,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
     }
   }
   // aliased nodes: unary, read by a regular (non-tail) kernel of the next layer
-  for (int nl = 1; nl < L && nl < tail; ++nl)
+  for (int nl = lo; nl < L && nl < tail; ++nl)
     for (int64_t i = 0; i < width(nl); ++i) {
       const int c = child[nl][i];
       if (c < 0) continue;
@@ -742,48 +753,70 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
   // mode 0: forward; 1: backward, log semiring (transposed CSR); 2: backward,
   // real semiring (product layers also need their forward CSR: zero-safe
   // adjoint). Returns the first layer of the longest qualifying suffix.
+  auto micro_ok = [&](int mode, int32_t l) {
+    const LayerDesc& d = p->layers[l];
+    const bool fwd = mode == 0;
+    const std::vector<int>& o = fwd ? off : toff;
+    const int64_t base = fwd ? d.off_base : d.toff_base, nodes = fwd ? d.W : d.Wprev;
+    int maxfan = 0;
+    for (int64_t i = 0; i < nodes; ++i) maxfan = std::max(maxfan, o[base + i + 1] - o[base + i]);
+    const int wmax = fwd ? MICRO_WF : MICRO_WB, cmax = fwd ? MICRO_CSRF : MICRO_CSRB;
+    const int64_t ints = nodes + 1 + d.E + ((mode == 2 && d.prod) ? d.W + 1 + d.E : 0);
+    return d.W <= wmax && d.Wprev <= wmax && maxfan <= MICRO_FAN && ints <= cmax;
+  };
+  // longest qualifying suffix (micro tail) and prefix below it (micro head;
+  // at least two layers, else a plain layer launch is as good)
   auto micro_suffix = [&](int mode) -> int32_t {
     int32_t mf = num_layers;
-    while (mf > 0 && num_layers - mf < MICRO_MAX_LAYERS) {
-      const LayerDesc& d = p->layers[mf - 1];
-      const bool fwd = mode == 0;
-      const std::vector<int>& o = fwd ? off : toff;
-      const int64_t base = fwd ? d.off_base : d.toff_base, nodes = fwd ? d.W : d.Wprev;
-      int maxfan = 0;
-      for (int64_t i = 0; i < nodes; ++i) maxfan = std::max(maxfan, o[base + i + 1] - o[base + i]);
-      const int wmax = fwd ? MICRO_WF : MICRO_WB, cmax = fwd ? MICRO_CSRF : MICRO_CSRB;
-      const int64_t ints = nodes + 1 + d.E + ((mode == 2 && d.prod) ? d.W + 1 + d.E : 0);
-      if (d.W > wmax || d.Wprev > wmax || maxfan > MICRO_FAN || ints > cmax) break;
-      --mf;
-    }
+    while (mf > 0 && num_layers - mf < MICRO_MAX_LAYERS && micro_ok(mode, mf - 1)) --mf;
     return mf;
+  };
+  // (head layers must be really thin, <= MICRO_HEAD_W nodes: wider bottom
+  // layers run faster as layer kernels spread over the whole GPU)
+  auto micro_head = [&](int mode, int32_t suffix) -> int32_t {
+    const int32_t lim = std::min(suffix, tail_from);  // below every tail
+    int32_t h = 0;
+    while (h < lim && h < MICRO_MAX_LAYERS && micro_ok(mode, h) &&
+           p->layers[h].W <= MICRO_HEAD_W && p->layers[h].Wprev <= MICRO_HEAD_W)
+      ++h;
+    return h >= 2 ? h : 0;
   };
   std::vector<int> micro, microb;
   p->micro_from = micro_suffix(0);
   p->microb_from = micro_suffix(1);
   p->microb_from_real = std::max(micro_suffix(2), p->microb_from);
-  for (int32_t l = p->micro_from; l < num_layers; ++l) {
-    const LayerDesc& d = p->layers[l];
-    p->micro_at.push_back((int)micro.size());
-    for (int64_t i = 0; i <= d.W; ++i) micro.push_back(off[d.off_base + i]);
-    for (int64_t e = 0; e < d.E; ++e) micro.push_back(src[d.e_base + e]);
-    p->micro_n.push_back((int)micro.size() - p->micro_at.back());
-    while (micro.size() % 4) micro.push_back(0);
-  }
-  // backward blocks: [transposed offsets, parents], then for product layers
-  // [forward offsets, children] (staged by the real semiring only)
-  for (int32_t l = p->microb_from; l < num_layers; ++l) {
-    const LayerDesc& d = p->layers[l];
-    p->microb_at.push_back((int)microb.size());
-    for (int64_t j = 0; j <= d.Wprev; ++j) microb.push_back(toff[d.toff_base + j]);
-    for (int64_t e = 0; e < d.E; ++e) microb.push_back(tpar[d.e_base + e]);
-    p->microb_n.push_back((int)microb.size() - p->microb_at.back());
-    if (d.prod) {
-      for (int64_t i = 0; i <= d.W; ++i) microb.push_back(off[d.off_base + i]);
-      for (int64_t e = 0; e < d.E; ++e) microb.push_back(src[d.e_base + e]);
+  p->head_f = micro_head(0, p->micro_from);
+  p->head_b = micro_head(1, p->microb_from);
+  p->head_b_real = std::min(micro_head(2, p->microb_from_real), p->head_b);
+  p->micro_at.assign(num_layers, -1);
+  p->micro_n.assign(num_layers, -1);
+  p->microb_at.assign(num_layers, -1);
+  p->microb_n.assign(num_layers, -1);
+  p->microbr_n.assign(num_layers, -1);
+  for (int32_t l = 0; l < num_layers; ++l) {
+    if (l < p->head_f || l >= p->micro_from) {
+      const LayerDesc& d = p->layers[l];
+      p->micro_at[l] = (int)micro.size();
+      for (int64_t i = 0; i <= d.W; ++i) micro.push_back(off[d.off_base + i]);
+      for (int64_t e = 0; e < d.E; ++e) micro.push_back(src[d.e_base + e]);
+      p->micro_n[l] = (int)micro.size() - p->micro_at[l];
+      while (micro.size() % 4) micro.push_back(0);
     }
-    p->microbr_n.push_back((int)microb.size() - p->microb_at.back());
-    while (microb.size() % 4) microb.push_back(0);
+    // backward blocks: [transposed offsets, parents], then for product
+    // layers [forward offsets, children] (staged by the real semiring only)
+    if (l < p->head_b || l >= p->microb_from) {
+      const LayerDesc& d = p->layers[l];
+      p->microb_at[l] = (int)microb.size();
+      for (int64_t j = 0; j <= d.Wprev; ++j) microb.push_back(toff[d.toff_base + j]);
+      for (int64_t e = 0; e < d.E; ++e) microb.push_back(tpar[d.e_base + e]);
+      p->microb_n[l] = (int)microb.size() - p->microb_at[l];
+      if (d.prod) {
+        for (int64_t i = 0; i <= d.W; ++i) microb.push_back(off[d.off_base + i]);
+        for (int64_t e = 0; e < d.E; ++e) microb.push_back(src[d.e_base + e]);
+      }
+      p->microbr_n[l] = (int)microb.size() - p->microb_at[l];
+      while (microb.size() % 4) microb.push_back(0);
+    }
   }
   if (num_layers >= 2 && row < (1LL << 30)) {
     build_aliases(p, num_inputs, widths, sources, segments, off, toff, tpar, aoff, aidx, omap,
@@ -846,6 +879,8 @@ extern "C" int klay_plan_schedule(const KlayPlan* p, int64_t* out) {
   out[1] = p->micro_from;
   out[2] = p->microb_from;
   out[3] = p->n_alias;
+  out[4] = p->head_f;
+  out[5] = p->head_b;
   return KLAY_OK;
 }
 extern "C" int64_t klay_plan_layer_offset(const KlayPlan* p, int32_t l) {
@@ -951,10 +986,47 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   // unary-sum aliases need the rows two layers down: backward-only traces
   constexpr bool U1_ = std::is_same<T, unsigned>::value;
   const bool alias = !U1_ && sr == SR_LOG_ && eps == 0.0 && retain_mode == 2 && !g_no_alias;
-  MicroArgs<T> micro{};
+  MicroArgs<T> micro{}, head{};
+  const int32_t head_f = (g_no_tail || g_no_micro || g_no_head || !micro_fits(V)) ? 0 : p->head_f;
+  auto run_micro = [&](MicroArgs<T>& m, int32_t first) -> int {
+    m.csr = p->d_micro;
+    m.V = V;
+    m.ld = ld;
+    m.eps = (T)eps;
+    LaunchScope ls(s, 6, first + 1);
+    int n;
+    if constexpr (U1) n = launch_forward_micro_u1(m, s);
+    else n = launch_forward_micro(sr, m, s);
+    if (n == 0) return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
+                                            cudaGetErrorString(cudaGetLastError()));
+    g_launches += n;
+    return KLAY_OK;
+  };
   for (int32_t l = 0; l < p->L; ++l) {
     const LayerDesc& d = p->layers[l];
     T* cur = retain ? values + (size_t)d.row * ld : pingpong[(l + 1) & 1];
+    if (l < head_f) {
+      // micro head: the thin bottom layers
+      const int i = head.n++;
+      if (i == 0) {
+        head.in = prev;
+        head.w_in = (int)d.Wprev;
+      }
+      head.out[i] = (retain || l == head_f - 1) ? cur : nullptr;
+      head.w[i] = (int)d.W;
+      head.csr_at[i] = p->micro_at[l];
+      head.csr_n[i] = p->micro_n[l];
+      head.prod[i] = d.prod ? 1 : 0;
+      if (l == head_f - 1) {
+        const int rc = run_micro(head, 0);
+        if (rc != KLAY_OK) {
+          delete tail;
+          return rc;
+        }
+      }
+      prev = cur;
+      continue;
+    }
     LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
     const bool redo = alias && d.fsum_redo;
     if (alias && d.fa_on) {
@@ -990,8 +1062,8 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       // ping-pong mode: only the last layer's rows are read afterwards
       micro.out[i] = (retain || l == p->L - 1) ? cur : nullptr;
       micro.w[i] = (int)d.W;
-      micro.csr_at[i] = p->micro_at[l - p->micro_from];
-      micro.csr_n[i] = p->micro_n[l - p->micro_from];
+      micro.csr_at[i] = p->micro_at[l];
+      micro.csr_n[i] = p->micro_n[l];
       micro.prod[i] = d.prod ? 1 : 0;
     } else if (l >= tail_from) {
       tail->layer[tail->n++] = a;
@@ -1031,17 +1103,8 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     if (g_tail_trace) tail_trace_dump("forward", micro_from - tail_from);
   }
   if (micro.n > 0) {
-    micro.csr = p->d_micro;
-    micro.V = V;
-    micro.ld = ld;
-    micro.eps = (T)eps;
-    LaunchScope ls(s, 6, micro_from + 1);
-    int n;
-    if constexpr (U1) n = launch_forward_micro_u1(micro, s);
-    else n = launch_forward_micro(sr, micro, s);
-    if (n == 0) return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
-                                            cudaGetErrorString(cudaGetLastError()));
-    g_launches += n;
+    const int rc = run_micro(micro, micro_from);
+    if (rc != KLAY_OK) return rc;
   }
   if (outputs && p->R > 0) {
     LaunchScope ls(s, 2, p->L + 1);
@@ -1084,7 +1147,9 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   // the backward micro tail covers the log semiring (pass / log-sum layers)
   const int32_t microb_from = (g_no_tail || g_no_micro || !micro_fits(V)) ? p->L
                                : (domain == SR_LOG_ ? p->microb_from : p->microb_from_real);
-  MicroBwdArgs<T> mb{};
+  const int32_t head_b = (g_no_tail || g_no_micro || g_no_head || !micro_fits(V)) ? 0
+                          : (domain == SR_LOG_ ? p->head_b : p->head_b_real);
+  MicroBwdArgs<T> mb{}, mh{};
   TailArgs<T>* tail = nullptr;
   if (tail_from < microb_from) {
     tail = new TailArgs<T>();
@@ -1103,31 +1168,38 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.unary_ok = (domain == SR_LOG_ && epsilon == 0.0) ? 1 : 0;
     a.rev = chunk_rev(l + 1);
     a.hcount = (l >= tail_from) ? nullptr : hcount;
-    if (l >= microb_from) {
-      const int i = mb.n++;
+    MicroBwdArgs<T>* cm = (l >= microb_from) ? &mb : (l < head_b ? &mh : nullptr);
+    if (cm) {
+      // micro tail (top) or micro head (bottom); the lowest layer of each is
+      // the one whose adjoints are read afterwards
+      const int32_t lowest = (cm == &mb) ? microb_from : 0;
+      MicroBwdArgs<T>& m = *cm;
+      const int i = m.n++;
       if (i == 0) {
-        mb.gin = a.gcur;
-        mb.w_top = (int)d.W;
+        m.gin = a.gcur;
+        m.w_top = (int)d.W;
       }
-      // only the lowest micro layer's adjoints are read afterwards
-      mb.gout[i] = (l == microb_from) ? a.out : nullptr;
-      mb.vpar[i] = a.ncur;
-      mb.vchild[i] = a.nprev;
-      mb.wp[i] = (int)d.W;
-      mb.wc[i] = (int)d.Wprev;
-      mb.csr_at[i] = p->microb_at[l - p->microb_from];
-      mb.csr_n[i] = (domain == SR_LOG_ ? p->microb_n : p->microbr_n)[l - p->microb_from];
+      m.gout[i] = (l == lowest) ? a.out : nullptr;
+      m.vpar[i] = a.ncur;
+      m.vchild[i] = a.nprev;
+      m.wp[i] = (int)d.W;
+      m.wc[i] = (int)d.Wprev;
+      m.csr_at[i] = p->microb_at[l];
+      m.csr_n[i] = (domain == SR_LOG_ ? p->microb_n : p->microbr_n)[l];
       // weighted layers: log sums (softmax weights), real products (zero-safe)
-      mb.logsum[i] = (domain == SR_LOG_) ? (d.prod ? 0 : 1) : (d.prod ? 1 : 0);
-      if (l == microb_from) {
-        mb.csr = p->d_microb;
-        mb.V = V;
-        mb.ld = ld;
-        mb.unary_ok = a.unary_ok;
-        LaunchScope ls(s, 7, microb_from + 1);
-        const int n = launch_backward_micro(domain, mb, s);
-        if (n == 0) return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
-                                                cudaGetErrorString(cudaGetLastError()));
+      m.logsum[i] = (domain == SR_LOG_) ? (d.prod ? 0 : 1) : (d.prod ? 1 : 0);
+      if (l == lowest) {
+        m.csr = p->d_microb;
+        m.V = V;
+        m.ld = ld;
+        m.unary_ok = a.unary_ok;
+        LaunchScope ls(s, 7, l + 1);
+        const int n = launch_backward_micro(domain, m, s);
+        if (n == 0) {
+          delete tail;
+          return fail(KLAY_ECUDA, std::string("micro-tail launch failed: ") +
+                                      cudaGetErrorString(cudaGetLastError()));
+        }
         g_launches += n;
       }
     } else if (l >= tail_from) {

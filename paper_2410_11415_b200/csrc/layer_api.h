@@ -78,6 +78,7 @@ constexpr int MICRO_P = 2;        // 16-byte pieces per CTA column chunk (32 byt
 constexpr int MICRO_WF = 2560;   // forward: two row sets of 32-byte chunks
 constexpr int MICRO_WB = 1280;   // backward: four row sets of 32-byte chunks
 constexpr int MICRO_FAN = 129;
+constexpr int MICRO_HEAD_W = 256;  // widths of micro-head layers (the thin bottom)
 constexpr int MICRO_CSRF = 8192;  // ints per staged layer CSR
 constexpr int MICRO_CSRB = 8192;
 template <typename T>

@@ -465,7 +465,7 @@ def test_alias_and_tail_extremes(cuda, tail_edges, no_micro):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("cfg", ["B", "C", "D", "E"])
+@pytest.mark.parametrize("cfg", ["A", "B", "C", "D", "E"])
 def test_plan_schedule_matches_byte_model(cuda, cfg):
     """bench.py's byte model restates the plan builder's schedule (tail and
     micro-tail boundaries) and its unary-node aliases; both must agree with
@@ -478,6 +478,8 @@ def test_plan_schedule_matches_byte_model(cuda, cfg):
     assert s["tail"] == bench._tail_from(tc)
     assert s["micro"] == bench._micro_from(tc, True)
     assert s["micro_bwd"] == bench._micro_from(tc, False)
+    assert s["head"] == bench._micro_head(tc, True)
+    assert s["head_bwd"] == bench._micro_head(tc, False)
     ap = bench.alias_plan(tc)
     n_alias = sum(int(np.asarray(a).sum()) for a in ap["ali"]) if ap is not None else 0
     assert s["aliased_rows"] == n_alias

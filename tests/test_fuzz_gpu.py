@@ -180,3 +180,66 @@ def test_micro_tail_pairwise_fanin(cuda, seed):
     ref, tr = oracle.forward(tc, lw, "log")
     rel_close(out.cpu().numpy(), ref, 1e-12, 1e-12)
     rel_close(g.cpu().numpy(), oracle.backward(tc, tr, "log"), 1e-12, 1e-12)
+
+
+def head_circuit(seed, K=48, W=40):
+    """Thin bottom layers (micro heads); layers 4 and 9 with a 300-edge
+    segment and a 140-parent child (layer kernels, heavy leaves) around
+    aliased layers; thin layers above (persistent / micro tails)."""
+    from paper_2410_11415_b200.tensorized import Literal, TensorizedCircuit, TensorLayer, validate
+    rng = np.random.default_rng(seed)
+    layers, prev = [], K
+    for l in range(13):
+        w = 2 if l == 12 else W
+        segs = [rng.integers(0, prev, size=int(rng.integers(1, 4))).tolist() for _ in range(w)]
+        if l in (4, 9):  # a 300-edge segment and a child read 140 times
+            segs[0].extend(rng.integers(0, prev, size=300).tolist())
+            segs[1].extend([0] * 140)
+        for c in range(prev):
+            segs[int(rng.integers(0, w))].append(c)
+        src = np.array([c for s in segs for c in s], np.int64)
+        seg = np.array([p for p, s in enumerate(segs) for _ in s], np.int64)
+        layers.append(TensorLayer("prod" if l % 2 == 0 else "sum", w, src, seg))
+        prev = w
+    input_map = {Literal(v, pos): 2 * (v - 1) + (0 if pos else 1)
+                 for v in range(1, K // 2 + 1) for pos in (True, False)}
+    tc = TensorizedCircuit(K, K // 2, layers, input_map, [0, 1], {})
+    validate(tc)
+    return tc
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_micro_heads(cuda, seed):
+    """Micro heads below layer kernels below a micro tail: real fp64
+    bit-exact, log fp64 within 1e-12 (values, gradients, every trace layer of
+    a backward-only trace, so aliases start above the heads)."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan
+    from paper_2410_11415_b200.engine import _NodeValues
+    tc = head_circuit(500 + seed)
+    plan = device_plan(tc)
+    assert plan.schedule["head"] >= 2 and plan.schedule["head_bwd"] >= 2
+    rng = np.random.default_rng(seed)
+    B = (1, 33, 128, 5)[seed]
+    w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
+    w[rng.uniform(size=w.shape) < 0.05] = 0.0
+    x = torch.tensor(w, dtype=torch.float64, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_REAL, np.float64)
+    g = plan.backward(vals, B, _lib.KLAY_REAL, np.float64)
+    ref, tr = oracle.forward(tc, w, "real")
+    assert np.array_equal(out.cpu().numpy(), ref, equal_nan=True)
+    np.testing.assert_array_equal(g.cpu().numpy(), oracle.backward(tc, tr, "real"))
+    with np.errstate(divide="ignore"):
+        lw = np.log(w)
+    x = torch.tensor(lw, dtype=torch.float64, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_LOG, np.float64)
+    g = plan.backward(vals, B, _lib.KLAY_LOG, np.float64)
+    with np.errstate(all="ignore"):
+        ref, tr = oracle.forward(tc, lw, "log")
+        gref = oracle.backward(tc, tr, "log")
+    rel_close(out.cpu().numpy(), ref, 1e-12, 1e-12)
+    rel_close(g.cpu().numpy(), gref, 1e-12, 1e-12)
+    nv = _NodeValues(plan, vals, B)
+    for l in range(len(tr)):
+        rel_close(nv[l], tr[l], 1e-12, 1e-12)
