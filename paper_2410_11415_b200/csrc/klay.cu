@@ -208,8 +208,13 @@ void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
 // sequential: it has no exact parallel decomposition).
 // cap shrinks for narrow layers so that thin layers still spread over many
 // warps (short per-warp dependency chains).
+// lse == true (forward log-sum layers): a logsumexp has no fixed summation
+// order to keep, so tails longer than LSE_SPLIT edges are split into ~8
+// equal leaves of 16..128 edges: a long segment spreads over several warps
+// instead of one long dependent exp chain.
+constexpr int LSE_SPLIT = 32;
 void build_items(const std::vector<int>& off, size_t base, int W, int short_max, ItemSet& s,
-                 bool split = true, int cap = 0) {
+                 bool split = true, int cap = 0, bool lse = false) {
   const int E = off[base + W] - off[base];
   if (cap <= 0) cap = std::max(short_max, std::min(TASK_EDGES_H, (E / 296) & ~7));
   std::vector<int4> leaves, longs, shorts;
@@ -236,10 +241,15 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   };
   for (int p = 0; p < W; ++p) {
     const int s0 = off[base + p], n = off[base + p + 1] - s0;
-    if (split && n - 1 > PW_BLOCK_H) {
+    if (split && n - 1 > (lse ? LSE_SPLIT : PW_BLOCK_H)) {
       flush(p);
       lv.clear();
-      split_leaves(s0 + 1, n - 1, lv);
+      if (lse) {
+        const int len = std::min(PW_BLOCK_H, std::max(16, (n - 1 + 7) / 8));
+        for (int a = s0 + 1; a < s0 + n; a += len) lv.push_back({a, std::min(a + len, s0 + n)});
+      } else {
+        split_leaves(s0 + 1, n - 1, lv);
+      }
       s.heavy.push_back(make_int4(p, s.slots, (int)lv.size(), 0));
       for (auto& l : lv) {
         leaves.push_back(make_int4(p, -(s.slots++) - 1, l.first, l.second));
@@ -280,6 +290,7 @@ struct LayerDesc {
   int64_t toff_base;      // into toff[] (Wprev+1 entries per layer)
   int64_t fi_base, fi_n, fh_base, fh_n, f_slots;  // forward items / heavy
   int64_t fq_base, fq_n;                           // forward items, no split (PROD)
+  int64_t fl_base, fl_n, flh_base, flh_n;          // forward items, log-sum leaves (LSE)
   int64_t bi_base, bi_n, bh_base, bh_n, b_slots;  // backward items / heavy
   // Unary-node aliases (log semiring, epsilon 0, backward-only traces; see
   // build_aliases). Per gate layer:
@@ -527,7 +538,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       d.fa.xmap_base = any_mrow ? (int64_t)omap.size() : -1;
       if (any_mrow) omap.insert(omap.end(), mr.begin(), mr.end());
       d.mrow_on = any_mrow;
-      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0);
+      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0, !d.prod);
       add_set(fa, d.fa, aoff, (size_t)d.fa.off_base, aidx, (size_t)d.fa.e_base);
       p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)fa.heavy.size());
@@ -722,6 +733,22 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       masks.insert(masks.end(), qs.masks.begin(), qs.masks.end());
       pad_items(qs.items, off, (size_t)d.off_base, src, (size_t)d.e_base);
     }
+    // log-sum layers with long segments: an item set with short leaves
+    d.fl_base = d.fi_base;
+    d.fl_n = 0;
+    ItemSet ls;
+    if (!d.prod && l < tail_from) {
+      int maxn = 0;
+      for (int64_t i = 0; i < W; ++i) maxn = std::max(maxn, off[d.off_base + i + 1] - off[d.off_base + i]);
+      if (maxn - 1 > LSE_SPLIT) {
+        build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, ls, true, 0, true);
+        d.fl_base = (int64_t)items.size();
+        d.fl_n = (int64_t)ls.items.size();
+        items.insert(items.end(), ls.items.begin(), ls.items.end());
+        masks.insert(masks.end(), ls.masks.begin(), ls.masks.end());
+        pad_items(ls.items, off, (size_t)d.off_base, src, (size_t)d.e_base);
+      }
+    }
     d.bi_base = (int64_t)items.size();
     d.bi_n = (int64_t)bs.items.size();
     items.insert(items.end(), bs.items.begin(), bs.items.end());
@@ -734,6 +761,11 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.bh_base = (int64_t)heavy.size();
     d.bh_n = (int64_t)bs.heavy.size();
     heavy.insert(heavy.end(), bs.heavy.begin(), bs.heavy.end());
+    d.flh_base = (int64_t)heavy.size();
+    d.flh_n = (int64_t)ls.heavy.size();
+    heavy.insert(heavy.end(), ls.heavy.begin(), ls.heavy.end());
+    p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ls.heavy.size());
+    p->max_fslots = std::max<int64_t>(p->max_fslots, ls.slots);
     d.f_slots = fs.slots;
     d.b_slots = bs.slots;
     p->max_fslots = std::max<int64_t>(p->max_fslots, fs.slots);
@@ -1037,6 +1069,16 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       if (d.fa.map_base >= 0) a.omap = p->d_omap + d.fa.map_base;
       if (d.fa.xmap_base >= 0) a.xmap = p->d_omap + d.fa.xmap_base;
       if (d.mrow_on) a.mbase = values;  // route masks (absolute rows)
+    }
+    if (sr == SR_LOG_ && !d.prod && d.fl_n > 0 && !(alias && d.fa_on)) {
+      // logsumexp: long segments split into short leaves
+      a.items = p->d_items + d.fl_base;
+      a.masks = p->d_masks + d.fl_base;
+      a.pidx = p->d_pidx + (size_t)d.fl_base * PADW_H;
+      a.poff = p->d_poff + (size_t)d.fl_base * PADW_H;
+      a.n_items = (int)d.fl_n;
+      a.heavy = p->d_heavy + d.flh_base;
+      a.n_heavy = (int)d.flh_n;
     }
     if (d.prod && (sr == SR_REAL_ || sr == KLAY_MAXPROD)) {
       // sequential product: heavy segments stay whole (no leaves, no combine)
