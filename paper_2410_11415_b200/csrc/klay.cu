@@ -213,6 +213,10 @@ void split_leaves(int a, int len, std::vector<std::pair<int, int>>& out) {
 // equal leaves of 16..128 edges: a long segment spreads over several warps
 // instead of one long dependent exp chain.
 constexpr int LSE_SPLIT = 32;
+const int LSE_LEAF_MIN = [] {  // (KLAY_LSE_LEAF: tuning experiments)
+  const char* e = getenv("KLAY_LSE_LEAF");
+  return (e && *e) ? std::max(1, atoi(e)) : 16;
+}();
 void build_items(const std::vector<int>& off, size_t base, int W, int short_max, ItemSet& s,
                  bool split = true, int cap = 0, bool lse = false) {
   const int E = off[base + W] - off[base];
@@ -245,7 +249,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
       flush(p);
       lv.clear();
       if (lse) {
-        const int len = std::min(PW_BLOCK_H, std::max(16, (n - 1 + 7) / 8));
+        const int len = std::min(PW_BLOCK_H, std::max(LSE_LEAF_MIN, (n - 1 + 7) / 8));
         for (int a = s0 + 1; a < s0 + n; a += len) lv.push_back({a, std::min(a + len, s0 + n)});
       } else {
         split_leaves(s0 + 1, n - 1, lv);

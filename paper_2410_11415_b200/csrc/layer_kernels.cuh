@@ -738,11 +738,22 @@ __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int 
     op.eps = a.eps;
     op.begin(n);
     op.push(x0);
-    for (int l = 0; l < nleaf; ++l) {
-      const Vec<T> pm = ldv(a.scratch + (size_t)(slot0 + l) * ld + col, nl);
-      const Vec<T> pt = ldv(a.scratch + a.tpart + (size_t)(slot0 + l) * ld + col, nl);
+    // leaf partials in groups of 4: the loads of a group are issued together
+    for (int l0 = 0; l0 < nleaf; l0 += 4) {
+      Vec<T> pm[4], pt[4];
 #pragma unroll
-      for (int c = 0; c < Vec<T>::N; ++c) lse_merge(op.m.v[c], op.t.v[c], pm.v[c], pt.v[c]);
+      for (int j = 0; j < 4; ++j) {
+        const int l = min(l0 + j, nleaf - 1);
+        pm[j] = ldv(a.scratch + (size_t)(slot0 + l) * ld + col, nl);
+        pt[j] = ldv(a.scratch + a.tpart + (size_t)(slot0 + l) * ld + col, nl);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (l0 + j < nleaf) {
+#pragma unroll
+          for (int c = 0; c < Vec<T>::N; ++c) lse_merge(op.m.v[c], op.t.v[c], pm[j].v[c], pt[j].v[c]);
+        }
+      }
     }
     res = op.result();
   } else {
