@@ -6,6 +6,7 @@ namespace klay {
 int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s) {
   switch (mode) {
     case BW_LOGSUM: return launch_layer<double, RK_SUM, BwdGather<double, BW_LOGSUM>>(a, s);
+    case BW_LOGSUM8: return launch_layer<double, RK_SUM, BwdGather<double, BW_LOGSUM8>>(a, s);
     case BW_REALPROD: return launch_layer<double, RK_SUM, BwdGather<double, BW_REALPROD>>(a, s);
     case BW_PASSA: return launch_layer<double, RK_SUM, BwdGather<double, BW_PASSA>>(a, s);
     default: return launch_layer<double, RK_SUM, BwdGather<double, BW_PASS>>(a, s);

@@ -21,7 +21,7 @@
 namespace klay {
 
 enum { SR_REAL = 0, SR_LOG = 1, SR_BOOL = 2, SR_MAXPROD = 3 };
-enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2, BW_PASSA = 3 };
+enum { BW_PASS = 0, BW_LOGSUM = 1, BW_REALPROD = 2, BW_PASSA = 3, BW_LOGSUM8 = 4 };
 // reduction kinds
 enum { RK_SUM = 0, RK_PROD = 1, RK_MAX = 2, RK_MIN = 3, RK_LSE = 4, RK_AND = 5, RK_OR = 6 };
 

@@ -22,7 +22,7 @@ using namespace klay;
 namespace {
 
 enum { SR_REAL_ = 0, SR_LOG_ = 1 };
-enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2, BW_PASSA_ = 3 };
+enum { BW_PASS_ = 0, BW_LOGSUM_ = 1, BW_REALPROD_ = 2, BW_PASSA_ = 3, BW_LOGSUM8_ = 4 };
 
 // work-item shape (see layer_kernels.cuh)
 #ifndef KLAY_TASK_EDGES
@@ -309,6 +309,7 @@ struct LayerDesc {
   //            absolute output rows (omap, bit 31: mask) and value rows (xmap)
   //   bmask    some outputs need the mask (pass-through layers: PASSA)
   bool fa_on, fsum_redo, mrow_on, ba_on, bmask;
+  bool bsum8;  // log-sum backward with 8-edge stage batches (children with > 4 parents common)
   AliasSet fa, ba;
 };
 
@@ -578,7 +579,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       omap.insert(omap.end(), outs.begin(), outs.end());
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
-      build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : SHORT_BWD_SUM, ba, true, 0);
+      build_items(aoff, (size_t)d.ba.off_base, (int)nc, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
+                  ba, true, 0);
       add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
@@ -720,7 +722,15 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
                                                    (TAIL_CLUSTER * TAIL_WARPS_H) + 7) & ~7))
         : 0;
     build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap);
-    build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : SHORT_BWD_SUM, bs, true, tcap);
+    // log-sum backward: 4-edge stage batches unless children with more
+    // parents are common (> 5 %), which would otherwise all become long items
+    if (!d.prod && l < tail_from) {
+      int64_t many = 0;
+      for (int64_t j = 0; j < prev_w; ++j) many += gcnt[j] > SHORT_BWD_SUM;
+      d.bsum8 = many * 20 > prev_w;
+    }
+    build_items(toff, (size_t)d.toff_base, (int)prev_w, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
+                bs, true, tcap);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
@@ -1277,7 +1287,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     } else {
       int mode = BW_PASS_;
       if (domain == SR_REAL_ && d.prod) mode = BW_REALPROD_;
-      else if (domain == SR_LOG_ && !d.prod) mode = BW_LOGSUM_;
+      else if (domain == SR_LOG_ && !d.prod) mode = d.bsum8 ? BW_LOGSUM8_ : BW_LOGSUM_;
       if (alias && d.ba_on) {
         // children whose adjoint is not routed; absolute output rows (route
         // tops write their chain's bottom) and value rows

@@ -114,17 +114,19 @@ struct FwdGather {
 template <typename T, int MODE>
 struct BwdGather {
   static constexpr bool PASSLIKE = (MODE == BW_PASS || MODE == BW_PASSA);
+  static constexpr bool LOGSUMLIKE = (MODE == BW_LOGSUM || MODE == BW_LOGSUM8);
   static constexpr int NOP = PASSLIKE ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   // (outputs flagged in omap carry the unary weight: own value or mask needed)
   static constexpr bool ROWV = (NOP == 2), MASKED_OUT = (NX == 1), ALIAS_IN = false;
   // edges per stage batch: log-sum layers stage three rows per edge and are
-  // shared-memory bound, so they use 4 (their segments are short)
+  // shared-memory bound, so they use 4 (their segments are short); layers
+  // whose children often have more parents use the 8-edge variant LOGSUM8
   static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : 8;
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
-                                                   : (MODE == BW_PASSA ? KLAY_PASS_MINB : 1));
+                                 : (MODE == BW_PASSA ? KLAY_PASS_MINB : (MODE == BW_LOGSUM8 ? 2 : 1)));
   const T* gbase;
   const T* nbase;
   const T* xbase;
@@ -142,7 +144,7 @@ struct BwdGather {
   // sum (klay.cu plan build); with epsilon 0 such a parent's value equals the
   // child's, so LOGSUM skips loading it (unary_ok) and every mode masks the bit.
   __device__ __forceinline__ bool unary_edge(int row) const {
-    return MODE == BW_LOGSUM && unary_ok && row < 0;
+    return LOGSUMLIKE && unary_ok && row < 0;
   }
   __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
     const size_t r = (size_t)(row & 0x7fffffff);
@@ -224,7 +226,7 @@ struct BwdGather {
                                             const Vec<T>& x) const {
     constexpr int N = Vec<T>::N;
     Vec<T> r;
-    if constexpr (MODE == BW_LOGSUM) {
+    if constexpr (LOGSUMLIKE) {
       r = logsum_edge(g, P, x);
     } else {
       // zero-safe product adjoint (engine.py:358-369): (g * prod) / x; a zero
