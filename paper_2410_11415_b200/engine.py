@@ -645,10 +645,11 @@ def gradient(tc, weights: WeightAssignment, log_domain: bool = False, epsilon: f
         sd = np.asarray(seed, dtype=np.dtype(dt))
         if sd.shape != (B, tc.num_roots):
             raise EvalError(f"seed must have shape {(B, tc.num_roots)}")
-    stream = torch.cuda.current_stream(plan.device)
-    cap.h_weights.numpy()[...] = w.values  # (idle: the previous call synchronized)
+    # (pinned buffers idle: the previous call synchronized; torch's copy_
+    # converts on several host threads)
+    cap.h_weights.copy_(torch.from_numpy(np.ascontiguousarray(w.values)))
     if seed is not None:
-        cap.h_seed.numpy()[...] = sd
+        cap.h_seed.copy_(torch.from_numpy(np.ascontiguousarray(sd)))
     cap.replay()  # H2D, forward, backward, D2H: one graph launch
-    stream.synchronize()
-    return cap.h_out.numpy().copy(), cap.h_grad.numpy().copy()
+    torch.cuda.current_stream(plan.device).synchronize()
+    return cap.h_out.clone().numpy(), cap.h_grad.clone().numpy()

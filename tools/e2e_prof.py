@@ -61,3 +61,19 @@ for _ in range(N):
                     ("sync", t4, t5), ("copyout", t5, t6)):
         acc[k] += (b - a) / N * 1e6
 print({k: round(v, 1) for k, v in acc.items()}, "dtype", W.values.dtype)
+# host copy variants
+wt = torch.from_numpy(W.values)
+hw = cap.h_weights
+def c_np():
+    hw.numpy()[...] = W.values
+def c_torch():
+    hw.copy_(wt)
+print("copyin numpy us", t(c_np, 200), "torch us", t(c_torch, 200), "threads", torch.get_num_threads())
+ho, hg = cap.h_out, cap.h_grad
+def o_np():
+    return ho.numpy().copy(), hg.numpy().copy()
+def o_torch():
+    return ho.clone().numpy(), hg.clone().numpy()
+def o_empty():
+    a = np.empty(hg.shape, np.float32); a[...] = hg.numpy(); b = np.empty(ho.shape, np.float32); b[...] = ho.numpy(); return b, a
+print("copyout numpy us", t(o_np, 200), "torch us", t(o_torch, 200), "empty+assign", t(o_empty, 200))
