@@ -220,6 +220,14 @@ def test_micro_heads(cuda, seed):
     tc = head_circuit(500 + seed)
     plan = device_plan(tc)
     assert plan.schedule["head"] >= 2 and plan.schedule["head_bwd"] >= 2
+    # no trace (ping-pong rows): every semiring through heads and tails
+    from paper_2410_11415_b200 import engine
+    rs = np.random.default_rng(50 + seed)
+    wr = rs.uniform(0.05, 0.95, size=(9, tc.num_inputs))
+    wb = (rs.uniform(size=wr.shape) < 0.6).astype(np.float64)
+    for sr, ww in (("real", wr), ("maxprod", wr), ("bool", wb)):
+        ref, _ = oracle.forward(tc, ww, sr, retain=False)
+        assert np.array_equal(engine.evaluate_semiring(tc, engine.WeightAssignment(ww), sr), ref), sr
     rng = np.random.default_rng(seed)
     B = (1, 33, 128, 5)[seed]
     w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
