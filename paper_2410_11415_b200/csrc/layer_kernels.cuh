@@ -19,21 +19,29 @@
 
 namespace klay {
 
+// One warp per block: a block's resources are released as soon as its one
+// item (of very uneven length) is done, so short and long items never hold
+// each other's SM slots (4-warp blocks: -7 %). The MINB values are resident
+// blocks (= warps) per SM the register budget is sized for; shared memory
+// (one stage per warp) caps the forward and pass-through kernels at 25.
 #ifndef KLAY_WARPS_PER_BLOCK
-#define KLAY_WARPS_PER_BLOCK 4
+#define KLAY_WARPS_PER_BLOCK 1
 #endif
 constexpr int WARPS_PER_BLOCK = KLAY_WARPS_PER_BLOCK;
 #ifndef KLAY_PASS_MINB
-#define KLAY_PASS_MINB 5  // resident blocks of the pass-through backward kernel
+#define KLAY_PASS_MINB 22  // resident blocks of the pass-through backward kernel
 #endif
 #ifndef KLAY_FWD_MINB
-#define KLAY_FWD_MINB 6
+#define KLAY_FWD_MINB 25
 #endif
 #ifndef KLAY_LOGSUM_SE
 #define KLAY_LOGSUM_SE 4
 #endif
 #ifndef KLAY_LOGSUM_MINB
-#define KLAY_LOGSUM_MINB 4
+#define KLAY_LOGSUM_MINB 18
+#endif
+#ifndef KLAY_LOGSUM8_MINB
+#define KLAY_LOGSUM8_MINB 8
 #endif
 
 
@@ -85,7 +93,7 @@ template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
-  static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 6)
+  static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
   const T* base;
   long long ld;
   int nl;
@@ -124,9 +132,10 @@ struct BwdGather {
   // whose children often have more parents use the 8-edge variant LOGSUM8
   static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : 8;
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
-  static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB            // (6 blocks: spills)
+  static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
-                                 : (MODE == BW_PASSA ? KLAY_PASS_MINB : (MODE == BW_LOGSUM8 ? 2 : 1)));
+                                 : (MODE == BW_PASSA ? KLAY_PASS_MINB
+                                                     : (MODE == BW_LOGSUM8 ? KLAY_LOGSUM8_MINB : 1)));
   const T* gbase;
   const T* nbase;
   const T* xbase;
