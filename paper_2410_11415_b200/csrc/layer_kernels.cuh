@@ -28,6 +28,10 @@ namespace klay {
 #define KLAY_WARPS_PER_BLOCK 1
 #endif
 constexpr int WARPS_PER_BLOCK = KLAY_WARPS_PER_BLOCK;
+#ifndef KLAY_CHUNKS_PER_WARP
+#define KLAY_CHUNKS_PER_WARP 1
+#endif
+constexpr int CHUNKS_PER_WARP = KLAY_CHUNKS_PER_WARP;
 #ifndef KLAY_PASS_MINB
 #define KLAY_PASS_MINB 22  // resident blocks of the pass-through backward kernel
 #endif
@@ -642,7 +646,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
       const int h = (int)ib->mask;
       __threadfence();
       __syncwarp();
-      int* cnt = a.hcount + (size_t)h * gridDim.y + chunk;
+      int* cnt = a.hcount + (size_t)h * ((a.V + 32 * NV - 1) / (32 * NV)) + chunk;
       int last = 0;
       if (lane == 0) last = atomicAdd(cnt, 1) == __ldg(&a.heavy[h].z) - 1;
       last = __shfl_sync(0xffffffffu, last, 0);
@@ -688,8 +692,16 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
 #endif
   store_item_regs(ib, r, lane);
   __syncwarp();
-  run_item<T, RK, G>(a, ib, a.rev ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y,
-                     reinterpret_cast<uint4*>(wbase), lane);
+  // CHUNKS_PER_WARP consecutive column chunks per warp share the index data
+  const int nch = (a.V + 32 * NV - 1) / (32 * NV);
+  const int gy = a.rev ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
+#pragma unroll 1
+  for (int k = 0; k < CHUNKS_PER_WARP; ++k) {
+    const int chunk = gy * CHUNKS_PER_WARP + (a.rev ? CHUNKS_PER_WARP - 1 - k : k);
+    if (chunk >= nch) continue;
+    if (k > 0) __syncwarp();  // the previous chunk is done with the stage
+    run_item<T, RK, G>(a, ib, chunk, reinterpret_cast<uint4*>(wbase), lane);
+  }
 }
 
 // KLAY_NO_PDL=1 launches layer kernels fully serialized (A/B switch)
@@ -813,7 +825,8 @@ inline int launch_layer(const LayerArgs<T>& a, cudaStream_t s) {
                            cudaSharedmemCarveoutMaxShared);
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK), chunks);
+    cfg.gridDim = dim3((unsigned)((a.n_items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK),
+                       (chunks + CHUNKS_PER_WARP - 1) / CHUNKS_PER_WARP);
     cfg.blockDim = dim3(WARPS_PER_BLOCK * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
