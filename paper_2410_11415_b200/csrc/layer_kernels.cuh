@@ -296,7 +296,10 @@ struct BwdGather {
 // into a double-buffered per-warp shared-memory stage, so a warp keeps up to
 // two batches of 512-byte row chunks in flight with no register cost.
 
-constexpr int TASK_EDGES = 128;  // max staged edge indices per item (longer items read idx directly)
+#ifndef KLAY_STAGED_IDX
+#define KLAY_STAGED_IDX 128
+#endif
+constexpr int TASK_EDGES = KLAY_STAGED_IDX;  // max staged edge indices per item (longer items read idx directly)
 constexpr int TASK_NODES = 31;   // max nodes of a short task (one lane per segment offset)
 
 // ---- per-item index data (warp-private shared memory) ----------------------
@@ -322,7 +325,11 @@ struct ItemsSmem {
   static constexpr int STAGE_V = SE * (EV + XV);   // pieces per stage
   static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * 16;
   // + one ItemIndex
-  static constexpr size_t warp_bytes = (stage_bytes + sizeof(ItemIndex) + 127) / 128 * 128;
+#ifndef KLAY_WARP_ALIGN
+#define KLAY_WARP_ALIGN 128
+#endif
+  static constexpr size_t warp_bytes =
+      (stage_bytes + sizeof(ItemIndex) + KLAY_WARP_ALIGN - 1) / KLAY_WARP_ALIGN * KLAY_WARP_ALIGN;
   static constexpr size_t bytes = warp_bytes * WARPS_PER_BLOCK;
 };
 
