@@ -28,6 +28,16 @@ namespace klay {
 #define KLAY_WARPS_PER_BLOCK 1
 #endif
 constexpr int WARPS_PER_BLOCK = KLAY_WARPS_PER_BLOCK;
+// staged edge indices per item (longer items read theirs from the plan):
+// backward / tail, and the forward policies (a smaller block leaves room for
+// one more resident warp: 23 instead of 22 per SM)
+#ifndef KLAY_STAGED_IDX
+#define KLAY_STAGED_IDX 128
+#endif
+#ifndef KLAY_FWD_STAGED_IDX
+#define KLAY_FWD_STAGED_IDX 96
+#endif
+constexpr int TASK_EDGES = KLAY_STAGED_IDX;
 #ifndef KLAY_CHUNKS_PER_WARP
 #define KLAY_CHUNKS_PER_WARP 1
 #endif
@@ -96,6 +106,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
+  static constexpr int CAP = KLAY_FWD_STAGED_IDX;  // staged edge indices per item
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
   const T* base;
@@ -127,6 +138,7 @@ template <typename T, int MODE>
 struct BwdGather {
   static constexpr bool PASSLIKE = (MODE == BW_PASS || MODE == BW_PASSA);
   static constexpr bool LOGSUMLIKE = (MODE == BW_LOGSUM || MODE == BW_LOGSUM8);
+  static constexpr int CAP = TASK_EDGES;  // staged edge indices per item
   static constexpr int NOP = PASSLIKE ? 1 : 2;
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   // (outputs flagged in omap carry the unary weight: own value or mask needed)
@@ -296,25 +308,27 @@ struct BwdGather {
 // into a double-buffered per-warp shared-memory stage, so a warp keeps up to
 // two batches of 512-byte row chunks in flight with no register cost.
 
-#ifndef KLAY_STAGED_IDX
-#define KLAY_STAGED_IDX 128
-#endif
-constexpr int TASK_EDGES = KLAY_STAGED_IDX;  // max staged edge indices per item (longer items read idx directly)
 constexpr int TASK_NODES = 31;   // max nodes of a short task (one lane per segment offset)
 
 // ---- per-item index data (warp-private shared memory) ----------------------
 // The structure of an item (descriptor, batch mask, edge indices, segment
 // offsets) does not depend on values: the tail kernel loads it for the next
 // layer while the cluster barrier of the current layer is still open.
-struct ItemIndex {
+// CAP: staged edge indices (a multiple of 32); longer items read theirs
+// from the plan. The forward policies use a smaller block (shared memory for
+// one more resident warp); the backward and the tail kernel use TASK_EDGES.
+template <int CAP>
+struct ItemIndexT {
+  static constexpr int cap = CAP;
   int4 it;            // item descriptor (see items_kernel)
   unsigned mask;      // short task: bit j set when node j starts a stage batch
   int pad[3];
-  int widx[TASK_EDGES];
+  int widx[CAP];
   int woff[32];       // short task: segment offsets relative to it.z
   int wmap[32];       // LayerArgs::omap entries of the item's nodes
   int wxmap[32];      // LayerArgs::xmap entries
 };
+using ItemIndex = ItemIndexT<TASK_EDGES>;
 
 template <typename T, typename G>
 struct ItemsSmem {
@@ -326,10 +340,10 @@ struct ItemsSmem {
   static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * 16;
   // + one ItemIndex
 #ifndef KLAY_WARP_ALIGN
-#define KLAY_WARP_ALIGN 128
+#define KLAY_WARP_ALIGN 16
 #endif
   static constexpr size_t warp_bytes =
-      (stage_bytes + sizeof(ItemIndex) + KLAY_WARP_ALIGN - 1) / KLAY_WARP_ALIGN * KLAY_WARP_ALIGN;
+      (stage_bytes + sizeof(ItemIndexT<G::CAP>) + KLAY_WARP_ALIGN - 1) / KLAY_WARP_ALIGN * KLAY_WARP_ALIGN;
   static constexpr size_t bytes = warp_bytes * WARPS_PER_BLOCK;
 };
 
@@ -356,13 +370,15 @@ __device__ __forceinline__ Vec<T> combine8(const Vec<T> (&r)[8]) {
 }
 
 // registers of one lane while an ItemIndex is in flight
-struct ItemRegs {
+template <int CAP>
+struct ItemRegsT {
   int4 it;
   unsigned mask;
-  int idx[TASK_EDGES / 32];
+  int idx[CAP / 32];
   int off;
   int map, xmap;
 };
+using ItemRegs = ItemRegsT<TASK_EDGES>;
 
 // Index data of item k (descriptor it/mask). Items with <= PADW edges have
 // their edge indices, raw segment offsets and maps in padded per-item rows
@@ -370,10 +386,10 @@ struct ItemRegs {
 // Longer items load their indices after the descriptor.
 constexpr int PADW = 32;
 
-template <typename T>
-__device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int k, int4 it,
-                                                   unsigned mask, int lane) {
-  ItemRegs r;
+template <typename T, int CAP = TASK_EDGES>
+__device__ __forceinline__ ItemRegsT<CAP> item_regs_from(const LayerArgs<T>& a, int k, int4 it,
+                                                         unsigned mask, int lane) {
+  ItemRegsT<CAP> r;
   r.it = it;
   r.mask = mask;
   const size_t pk = (size_t)k * PADW + lane;
@@ -385,30 +401,31 @@ __device__ __forceinline__ ItemRegs item_regs_from(const LayerArgs<T>& a, int k,
   if (ne <= PADW) {
     r.idx[0] = p0;
 #pragma unroll
-    for (int q = 1; q < TASK_EDGES / 32; ++q) r.idx[q] = 0;
+    for (int q = 1; q < CAP / 32; ++q) r.idx[q] = 0;
   } else {
 #pragma unroll
-    for (int q = 0; q < TASK_EDGES / 32; ++q) {
+    for (int q = 0; q < CAP / 32; ++q) {
       const int e = q * 32 + lane;
-      r.idx[q] = (ne <= TASK_EDGES && e < ne) ? __ldg(a.idx + r.it.z + e) : 0;
+      r.idx[q] = (ne <= CAP && e < ne) ? __ldg(a.idx + r.it.z + e) : 0;
     }
   }
   r.off = r.it.y > 0 ? o0 - r.it.z : 0;  // segment offsets relative to the first edge
   return r;
 }
 
-template <typename T>
-__device__ __forceinline__ ItemRegs load_item_regs(const LayerArgs<T>& a, int item, int lane) {
-  return item_regs_from(a, item, __ldg(a.items + item), __ldg(a.masks + item), lane);
+template <typename T, int CAP = TASK_EDGES>
+__device__ __forceinline__ ItemRegsT<CAP> load_item_regs(const LayerArgs<T>& a, int item, int lane) {
+  return item_regs_from<T, CAP>(a, item, __ldg(a.items + item), __ldg(a.masks + item), lane);
 }
 
-__device__ __forceinline__ void store_item_regs(ItemIndex* ib, const ItemRegs& r, int lane) {
+template <int CAP>
+__device__ __forceinline__ void store_item_regs(ItemIndexT<CAP>* ib, const ItemRegsT<CAP>& r, int lane) {
   if (lane == 0) {
     ib->it = r.it;
     ib->mask = r.mask;
   }
 #pragma unroll
-  for (int q = 0; q < TASK_EDGES / 32; ++q) ib->widx[q * 32 + lane] = r.idx[q];
+  for (int q = 0; q < CAP / 32; ++q) ib->widx[q * 32 + lane] = r.idx[q];
   ib->woff[lane] = r.off;
   ib->wmap[lane] = r.map;
   ib->wxmap[lane] = r.xmap;
@@ -436,8 +453,8 @@ template <typename T, int RK, typename G>
 __device__ __forceinline__ void process_heavy(const LayerArgs<T>& a, int h, int chunk, int lane,
                                               uint4* sm, int sm_pieces);
 
-template <typename T, int RK, typename G>
-__device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex* ib, int chunk,
+template <typename T, int RK, typename G, int CAP>
+__device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT<CAP>* ib, int chunk,
                                          uint4* stage, int lane) {
   using S = ItemsSmem<T, G>;
   constexpr int SE = S::SE, EV = S::EV, XV = S::XV, STAGE_V = S::STAGE_V;
@@ -455,7 +472,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndex*
   const int4 it = ib->it;
   const int ne = it.w - it.z;
   const G g(a, col, lc.nl);
-  const bool staged_idx = ne <= TASK_EDGES;
+  const bool staged_idx = ne <= CAP;
 
   if (it.y > 0) {
     // ======================= short task =======================
@@ -688,11 +705,11 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
   const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
   if (item >= a.n_items) return;  // no block-wide barriers inside
   unsigned char* wbase = smem + (size_t)warp * S::warp_bytes;
-  ItemIndex* ib = reinterpret_cast<ItemIndex*>(wbase + S::stage_bytes);
+  ItemIndexT<G::CAP>* ib = reinterpret_cast<ItemIndexT<G::CAP>*>(wbase + S::stage_bytes);
   // The item's index data is plan data: load it before waiting on the
   // previous layer's kernel (programmatic dependent launch, launch_layer),
   // and let the next layer's blocks start their own prologue meanwhile.
-  const ItemRegs r = load_item_regs(a, item, lane);
+  const ItemRegsT<G::CAP> r = load_item_regs<T, G::CAP>(a, item, lane);
 #ifndef KLAY_NO_GDC
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -707,7 +724,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
     const int chunk = gy * CHUNKS_PER_WARP + (a.rev ? CHUNKS_PER_WARP - 1 - k : k);
     if (chunk >= nch) continue;
     if (k > 0) __syncwarp();  // the previous chunk is done with the stage
-    run_item<T, RK, G>(a, ib, chunk, reinterpret_cast<uint4*>(wbase), lane);
+    run_item<T, RK, G, G::CAP>(a, ib, chunk, reinterpret_cast<uint4*>(wbase), lane);
   }
 }
 
@@ -881,9 +898,10 @@ struct TailDesc {
 // per warp: stage sized for the larger policy, one ItemIndex, the descriptor table
 template <typename T, typename GP, typename GS>
 struct TailSmem {
-  static constexpr size_t item_bytes = ItemsSmem<T, GP>::warp_bytes > ItemsSmem<T, GS>::warp_bytes
-                                           ? ItemsSmem<T, GP>::warp_bytes
-                                           : ItemsSmem<T, GS>::warp_bytes;
+  static constexpr size_t stage_max = ItemsSmem<T, GP>::stage_bytes > ItemsSmem<T, GS>::stage_bytes
+                                         ? ItemsSmem<T, GP>::stage_bytes
+                                         : ItemsSmem<T, GS>::stage_bytes;
+  static constexpr size_t item_bytes = (stage_max + sizeof(ItemIndex) + 127) / 128 * 128;
   static constexpr size_t warp_bytes = item_bytes + sizeof(TailDesc) * TAIL_MAX_LAYERS;
   // as many warps (<= TAIL_WARPS) as fit the 227 KB of shared memory
   static constexpr int warps = (227 * 1024) / warp_bytes < TAIL_WARPS ? (int)((227 * 1024) / warp_bytes)
