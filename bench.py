@@ -65,7 +65,7 @@ def _tail_from(tc):
 
 def _micro_ok(tc, l, fwd):
     widths = [tc.num_inputs] + [x.width for x in tc.layers]
-    wmax = 2560 if fwd else 1280
+    wmax = 1280
     layer = tc.layers[l]
     W, Wp, E = widths[l + 1], widths[l], len(layer.sources)
     key = layer.segments if fwd else layer.sources
@@ -89,7 +89,7 @@ def _micro_head(tc, fwd):
 
 def _micro_from(tc, fwd):
     """First layer of libklay's forward / backward micro tail (klay.cu
-    micro_suffix: longest suffix of <= 64 layers with widths <= 2560 / 1280,
+    micro_suffix: longest suffix of <= 64 layers with widths <= 1280,
     fan-in / fan-out <= 129 and one layer's CSR <= 8192 ints; log semiring)."""
     L = len(tc.layers)
     m = L

@@ -75,7 +75,10 @@ struct TailArgs {
 // aligned offset of one plan int array and staged per layer.
 constexpr int MICRO_MAX_LAYERS = 64;
 constexpr int MICRO_P = 2;        // 16-byte pieces per CTA column chunk (32 bytes)
-constexpr int MICRO_WF = 2560;   // forward: two row sets of 32-byte chunks
+#ifndef KLAY_MICRO_WF
+#define KLAY_MICRO_WF 1280
+#endif
+constexpr int MICRO_WF = KLAY_MICRO_WF;  // forward: two row sets of 32-byte chunks
 constexpr int MICRO_WB = 1280;   // backward: four row sets of 32-byte chunks
 constexpr int MICRO_FAN = 129;
 constexpr int MICRO_HEAD_W = 256;  // widths of micro-head layers (the thin bottom)
