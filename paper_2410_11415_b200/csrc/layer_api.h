@@ -79,7 +79,10 @@ constexpr int MICRO_P = 2;        // 16-byte pieces per CTA column chunk (32 byt
 #define KLAY_MICRO_WF 1280
 #endif
 constexpr int MICRO_WF = KLAY_MICRO_WF;  // forward: two row sets of 32-byte chunks
-constexpr int MICRO_WB = 1280;   // backward: four row sets of 32-byte chunks
+#ifndef KLAY_MICRO_WB
+#define KLAY_MICRO_WB 1280
+#endif
+constexpr int MICRO_WB = KLAY_MICRO_WB;  // backward: four row sets of 32-byte chunks
 constexpr int MICRO_FAN = 129;
 constexpr int MICRO_HEAD_W = 256;  // widths of micro-head layers (the thin bottom)
 constexpr int MICRO_CSRF = 8192;  // ints per staged layer CSR
