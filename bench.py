@@ -2,21 +2,23 @@
 
 Workload (BASELINE.json configs[2]): the 1,016,536-node
 d-DNNF compiled from gen_3cnf(56, 128, seed 1) (data/circuits/C.npz), log
-semiring fp32, 1024 batch rows per GPU (weak scaling), Philox(key=0) weights
-p ~ U(0.05, 0.95) per literal. One step = forward (trace retained) +
-backward (all-ones seed) over one batch; with N > 1 ranks each rank owns its
-own 1024 rows and the root outputs are all-gathered over NCCL.
+semiring fp32, global batch 1024 sharded over the N GPUs (strong scaling, the
+north star's "batch 1024 at 1/2/4/8 B200"; `--scaling weak` gives every GPU
+its own 1024 rows), Philox(key=0) weights p ~ U(0.05, 0.95) per literal. One
+step = forward (trace retained) + backward (all-ones seed) of this rank's rows
+as one CUDA-graph replay, then NCCL all-gathers of the outputs [B, R] and the
+input gradients [B, K] (distributed.ShardedPass).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Rank 0 prints ONE JSON line. `value` = device-timed evals/s with inputs
-resident in HBM (CUDA events, max over ranks); `e2e` = the same metric
-through the public API (engine.forward_log + engine.backward with host numpy
-arrays; H2D of the weights and D2H of roots + grads inside the timed region);
-`roofline` = the dominant kernel's algorithmic bytes / its event-timed
-duration (per-launch CUDA events in a separate instrumented step);
+`--gpus N` outside torchrun re-launches itself as N ranks. Rank 0 prints ONE
+JSON line. `value` = device-timed evals/s with inputs resident in HBM (CUDA
+events, max over ranks); `e2e` = the same metric through the public API
+(engine.gradient with host numpy arrays on each rank's rows, gathered);
+`roofline` = per launch class (template) the bytes the implemented dataflow
+must move over its in-graph time (time_classes), the dominant class on top;
 `cpu_baseline` = the CPU oracle (numpy restatement of the reference engine)
-on this host's cores.
+on this host's cores, with the single-process figure beside it.
 """
 
 from __future__ import annotations
@@ -320,6 +322,185 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# per-template (launch class) byte model and in-graph timing
+# ---------------------------------------------------------------------------
+
+# launch classes of libklay (include/klay.h KLAY_CLASS_*)
+CLASS_NAMES = ["fwd_prod", "fwd_sum", "bwd_pass", "bwd_logsum", "bwd_realprod",
+               "fwd_micro", "bwd_micro", "tail", "boundary"]
+
+
+def kernel_class(name, domain="log"):
+    """Launch class of an ncu kernel name (log semiring: product layers
+    reduce with RK_SUM = 0, sum layers with RK_LSE = 4)."""
+    n = name.replace("void ", "")
+    if n.startswith(("items_kernel", "combine_kernel")):
+        args = n[n.index("<") + 1:].split(",")
+        if "BwdGather" in n:
+            mode = int(n.split("BwdGather<")[1].split(",")[1].split(">")[0])
+            return {0: "bwd_pass", 3: "bwd_pass", 1: "bwd_logsum", 4: "bwd_logsum",
+                    2: "bwd_realprod"}[mode]
+        rk = int(args[1])
+        if domain == "log":
+            return "fwd_prod" if rk == 0 else "fwd_sum"
+        return "fwd_prod" if rk == 1 else "fwd_sum"
+    if n.startswith("micro_bwd_kernel"):
+        return "bwd_micro"
+    if n.startswith("micro_kernel"):
+        return "fwd_micro"
+    if n.startswith("tail_kernel"):
+        return "tail"
+    return "boundary"
+
+
+def schedule(plan, B, s):
+    """Which gate layers (0-based) run in which launch class at batch B
+    (klay.cu forward_impl / backward_impl; micro tails and heads only when
+    their grid fits two waves, klay.cu micro_fits)."""
+    import torch
+    L = plan.num_layers
+    ld = plan.row_stride(B, np.float64 if s == 8 else np.float32)
+    V = ld * s // 16
+    sms = torch.cuda.get_device_properties(plan.device).multi_processor_count
+    ok = (V + 1) // 2 <= 2 * sms
+    sc = plan.schedule
+    micro = sc["micro"] if ok else L
+    microb = sc["micro_bwd"] if ok else L
+    head = sc["head"] if ok else 0
+    headb = sc["head_bwd"] if ok else 0
+    tail = sc["tail"]
+    fwd = {}
+    for l in range(L):
+        fwd[l] = ("fwd_micro" if (l < head or l >= micro) else
+                  "tail" if l >= tail else None)
+    bwd = {}
+    for l in range(L):
+        bwd[l] = ("bwd_micro" if (l < headb or l >= microb) else
+                  "tail" if l >= tail else None)
+    return fwd, bwd, dict(micro=micro, microb=microb, head=head, headb=headb, tail=tail)
+
+
+def class_bytes(tc, plan, B, s):
+    """Per launch class: (necessary bytes per step, SURVEY-model bytes per
+    step, layer list). Layer kernels use layer_bytes / survey_layer_bytes;
+    the micro tails and heads move their first layer's input rows, every
+    stored output row and their CSR (forward), or the top adjoints, the
+    weighted (log-sum) layers' value rows, the lowest adjoints and the CSR
+    (backward); boundary kernels the [B,K] / [B,R] host-layout tensors."""
+    fwd_n, bwd_n = layer_bytes(tc, s, B)
+    fwd_s, bwd_s = survey_layer_bytes(tc, s, B)
+    fcls, bcls, sc = schedule(plan, B, s)
+    row = s * B
+    widths = [tc.num_inputs] + [l.width for l in tc.layers]
+    nec = {c: 0.0 for c in CLASS_NAMES}
+    sur = {c: 0.0 for c in CLASS_NAMES}
+    layers = {c: [] for c in CLASS_NAMES}
+    micro_f, micro_b = [], []
+    for l, layer in enumerate(tc.layers):
+        E = len(layer.sources)
+        c = fcls[l] or ("fwd_prod" if layer.op == "prod" else "fwd_sum")
+        layers[c].append(l)
+        sur[c] += fwd_s[l + 1]
+        if c == "fwd_micro":
+            micro_f.append(l)
+            nec[c] += row * widths[l + 1] + 4 * (widths[l + 1] + 1 + E)
+        else:
+            nec[c] += fwd_n[l + 1]
+        c = bcls[l] or ("bwd_pass" if layer.op == "prod" else "bwd_logsum")
+        layers[c].append(l)
+        sur[c] += bwd_s[l + 1]
+        if c == "bwd_micro":
+            micro_b.append(l)
+            weighted = layer.op != "prod"
+            nec[c] += (row * (widths[l + 1] + widths[l]) if weighted else 0) \
+                + 4 * (widths[l] + 1 + E)
+        else:
+            nec[c] += bwd_n[l + 1]
+    # input rows of each forward micro launch, output adjoints of each backward one
+    for lo in (0, sc["micro"]):
+        if lo in micro_f:
+            nec["fwd_micro"] += row * widths[lo]
+    for top, low in ((sc["headb"] - 1, 0), (len(tc.layers) - 1, sc["microb"])):
+        if top in micro_b:
+            nec["bwd_micro"] += row * (widths[top + 1] + widths[low])
+    K, R = tc.num_inputs, tc.num_roots
+    nec["boundary"] = sur["boundary"] = 2 * row * (K + R) + row * widths[-1]
+    return nec, sur, layers
+
+
+def time_classes(lib, run_step, iters=20):
+    """In-graph device time per launch class: one CUDA graph per class
+    holding only that class's launches of a full step (klay_set_launch_filter),
+    replayed `iters` times between CUDA events. Work is data-independent in
+    the log semiring, so a class times the same as inside the full graph
+    (up to its neighbours' overlap through programmatic dependent launch)."""
+    import torch
+    out = {}
+    for c, name in enumerate(CLASS_NAMES):
+        prev = lib.klay_set_launch_filter(1 << c)
+        n0 = lib.klay_launch_count()
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                run_step()
+        finally:
+            lib.klay_set_launch_filter(prev)
+        n = lib.klay_launch_count() - n0
+        if n == 0:
+            continue
+        for _ in range(3):
+            g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = {"launches": int(n), "ms": e0.elapsed_time(e1) / iters}
+        del g
+    return out
+
+
+def ncu_class_traffic(path, domain="log"):
+    """Per launch class from a committed ncu launch list (profiles/):
+    DRAM read+write bytes and device time per step, launches per step."""
+    import csv
+    if not os.path.exists(path):
+        return None
+    rows = list(csv.reader(open(path)))
+    try:
+        hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    except IndexError:
+        return None
+    h = rows[hi]
+    ik, im, iu, iv = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Unit",
+                                           "Metric Value"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
+             "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}
+    per = {}
+    ids = {}
+    for r in rows[hi + 1:]:
+        if len(r) <= iv:
+            continue
+        c = kernel_class(r[ik], domain)
+        d = per.setdefault(c, {"dram_bytes": 0.0, "ms": 0.0})
+        v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1)
+        if r[im].startswith("dram__bytes"):
+            d["dram_bytes"] += v
+        elif r[im] == "gpu__time_duration.sum":
+            d["ms"] += v * 1e3
+        ids.setdefault(c, set()).add(r[0])
+    steps = 1
+    meta = path[:-4] + ".json"
+    if os.path.exists(meta):
+        with open(meta) as fh:
+            steps = json.load(fh).get("steps", 1)
+    return {c: {"dram_bytes": d["dram_bytes"] / steps, "ms": d["ms"] / steps,
+                "launches": len(ids[c]) // steps} for c, d in per.items()}
+
+
+# ---------------------------------------------------------------------------
 # CPU oracle timing (reference arm and cpu_baseline)
 # ---------------------------------------------------------------------------
 
@@ -346,7 +527,7 @@ def _worker_run(args):
     return rows, time.perf_counter() - t0
 
 
-def cpu_pool_size(per_worker_gb=1.0):
+def cpu_pool_size(per_worker_gb=1.5):
     n = os.cpu_count() or 1
     try:
         import psutil
@@ -370,8 +551,17 @@ class CpuOracle:
         self.pool = ctx.Pool(self.procs, initializer=_worker_init, initargs=(path,))
         self.pool.map(_worker_run, [(i, 1) for i in range(self.procs)])  # warm plans
 
-    def step(self, tasks_per_proc=1, seed0=0):
-        tasks = [(seed0 + i, self.rows) for i in range(self.procs * tasks_per_proc)]
+    def step(self, rows, seed0=0):
+        """`rows` rows split into one task per process (the last ones
+        shorter); returns (rows, wall seconds)."""
+        per = -(-rows // self.procs)
+        tasks = []
+        left = rows
+        i = 0
+        while left > 0:
+            tasks.append((seed0 + i, min(per, left)))
+            left -= per
+            i += 1
         t0 = time.perf_counter()
         res = self.pool.map(_worker_run, tasks, chunksize=1)
         wall = time.perf_counter() - t0
@@ -382,19 +572,41 @@ class CpuOracle:
         self.pool.join()
 
 
+def single_process_cpu(seconds, rows=64):
+    """The reference's own arrangement (bench.py:177-183 of the reference:
+    one process, single-threaded numpy): evals/s of the oracle port in this
+    process on `rows`-row chunks for about `seconds`."""
+    _worker_init(CIRCUIT)
+    _worker_run((5, 1))
+    done = wall = 0.0
+    i = 0
+    while wall < seconds or i == 0:
+        r, t = _worker_run((500 + i, rows))
+        done += r
+        wall += t
+        i += 1
+    return {"value": done / wall, "unit": "evals/s", "cores": 1, "kind": "port",
+            "sample": f"{int(done)} rows of config C in {wall:.1f} s, one process, "
+                      f"{rows}-row chunks, oracle/engine_port.py, fp32 log fwd+bwd"}
+
+
 def run_reference_arm(args):
+    """The reference's CPU engine (oracle port, same ufunc sequence as
+    laycirc/engine.py) on the GPU arm's workload: each step is the same
+    1024-row config C fwd+bwd, split over one process per core."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0  # rank 0 alone runs the CPU reference
     from paper_2410_11415_b200.tensorized import load_npz
     tc = load_npz(CIRCUIT)
+    single = single_process_cpu(args.cpu_single_seconds)
     cpu = CpuOracle(CIRCUIT)
     for i in range(args.warmup):
-        cpu.step(seed0=1000 * i)
+        cpu.step(cpu.procs, seed0=1000 * i)  # untimed warm-up: one row per process
     rows = 0
     wall = 0.0
     for i in range(args.steps):
-        r, t = cpu.step(seed0=10_000 + 1000 * i)
+        r, t = cpu.step(args.batch, seed0=10_000 + 1000 * i)
         rows += r
         wall += t
     cpu.close()
@@ -403,16 +615,18 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "nodes": nodes,
                    "edges": int(sum(len(l.sources) for l in tc.layers)),
-                   "semiring": "log", "pass": "fwd+bwd",
-                   "rows_per_step": cpu.procs * cpu.rows},
+                   "semiring": "log", "pass": "fwd+bwd", "global_batch": args.batch,
+                   "rows_per_step": args.batch,
+                   "warmup_rows": f"{cpu.procs} (one per process: warms the plans)"},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cpu.procs, "kind": "port",
-                         "sample": f"{cpu.procs} processes x {cpu.rows} rows per step, "
-                                   "oracle/engine_port.py (numpy restatement of "
-                                   "laycirc/engine.py), fp32 log fwd+bwd"},
+                         "sample": f"{args.steps} steps x {args.batch} rows ({cpu.procs} "
+                                   "processes, one chunk each), oracle/engine_port.py (numpy "
+                                   "restatement of laycirc/engine.py), fp32 log fwd+bwd",
+                         "single_process": single},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -424,8 +638,22 @@ def run_reference_arm(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def _timed_replays(fn, n, dev):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(n):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / n
+
+
 def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
-    """Device-timed evals/s of another BASELINE config (inputs in HBM)."""
+    """Device-timed evals/s of another BASELINE config (inputs in HBM; one
+    CUDA-graph replay per batch, like the headline)."""
     import torch
     from paper_2410_11415_b200 import _lib, engine
     from paper_2410_11415_b200.tensorized import load_npz
@@ -451,17 +679,19 @@ def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
         if with_backward:
             plan.backward(vals, B, code, dtype, workspace=work)
 
+    for _ in range(2):
+        step()
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
     for _ in range(3):
-        step()
-    stream = torch.cuda.current_stream(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize(dev)
-    e0.record(stream)
-    for _ in range(iters):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / iters
+        g.replay()
+    ms = _timed_replays(g.replay, iters, dev)
     s = 8 if dtype == np.float64 else (1 / 8 if dtype == "u1" else 4)
     dom = semiring if semiring in ("log", "real") else "log"
     fwd_b, bwd_b = survey_layer_bytes(tc, s, B, dom)
@@ -470,11 +700,25 @@ def measure_config(name, semiring, dtype, B, with_backward, dev, iters=20):
     nec = sum(fwd_n.values()) + (sum(bwd_n.values()) if with_backward else 0)
     peak, _ = load_peaks()
     nodes = tc.num_inputs + sum(l.width for l in tc.layers)
+    del g
     return {"nodes": nodes, "semiring": semiring,
             "dtype": {8: "f64", 4: "f32"}.get(s, "u1 (bit-packed)"), "batch": B,
             "pass": "fwd+bwd" if with_backward else "fwd", "ms_per_batch": ms,
-            "evals_per_s": B / (ms / 1e3), "roofline_frac": alg / (ms / 1e3) / 1e9 / peak,
+            "evals_per_s": B / (ms / 1e3), "contract_frac": alg / (ms / 1e3) / 1e9 / peak,
             "frac_necessary": nec / (ms / 1e3) / 1e9 / peak}
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N
+    ranks (torch.distributed.run, 127.0.0.1); rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def run_gpu_arm(args):
@@ -484,88 +728,82 @@ def run_gpu_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world
-    from paper_2410_11415_b200 import engine, _lib
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)",
+              file=sys.stderr)
+    from paper_2410_11415_b200 import _lib, engine
+    from paper_2410_11415_b200.distributed import ShardedPass, sharded_eval
     from paper_2410_11415_b200.tensorized import load_npz
 
     tc = load_npz(CIRCUIT)
-    B = args.batch
     s = 4  # fp32
     dt = np.float32
+    strong = args.scaling == "strong"
+    B_global = args.batch if strong else args.batch * world
 
-    # CPU baseline first (rank 0, N = 1 only), before CUDA is initialised,
+    # CPU baselines first (rank 0, N = 1 only), before CUDA is initialised,
     # so the fork pool never inherits a CUDA context.
     cpu_line = None
     if world == 1 and not args.no_cpu_baseline:
+        single = single_process_cpu(args.cpu_single_seconds)
         cpu = CpuOracle(CIRCUIT)
-        cpu.step(seed0=77)
         rows = wall = 0
         t_end = time.perf_counter() + args.cpu_seconds
         i = 0
         while time.perf_counter() < t_end or i == 0:
-            r, t = cpu.step(seed0=100 + 1000 * i)
+            r, t = cpu.step(cpu.procs * cpu.rows, seed0=100 + 1000 * i)
             rows += r
             wall += t
             i += 1
         cpu.close()
         cpu_line = {"value": rows / wall, "unit": "evals/s", "cores": cpu.procs, "kind": "port",
                     "sample": f"{rows} rows of config C in {wall:.1f} s ({cpu.procs} processes x "
-                              f"{cpu.rows}-row chunks), oracle/engine_port.py, fp32 log fwd+bwd"}
+                              f"{cpu.rows}-row chunks), oracle/engine_port.py, fp32 log fwd+bwd",
+                    "single_process": single}
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
-    plan = engine.device_plan(tc, dev)
 
     rng = np.random.Generator(np.random.Philox(key=0))
-    w_all = np.log(rng.uniform(0.05, 0.95, size=(B * world, tc.num_inputs)))
-    w_host = w_all[rank * B:(rank + 1) * B]
-    w_dev = torch.from_numpy(w_host.astype(np.float32)).to(dev)
-    values = plan.alloc_values(B, dt, retain=True)
-    outputs = torch.empty((B, tc.num_roots), dtype=torch.float32, device=dev)
-    grads = torch.empty((B, tc.num_inputs), dtype=torch.float32, device=dev)
-    work = plan.workspace(B, dt)
-    gathered = [torch.empty_like(outputs) for _ in range(world)] if world > 1 else None
-    launches_per_step = None
+    w_all = np.log(rng.uniform(0.05, 0.95, size=(B_global, tc.num_inputs)))
 
-    # the timed step replays one CUDA graph holding the whole fwd + bwd
-    # (~100 kernels for config C); the instrumented step below launches them
-    # one by one on the stream to time each
-    cap = plan.capture(B, dt, _lib.KLAY_LOG, backward=True)
-    cap.weights.copy_(w_dev)
+    # one step: a CUDA-graph replay of this rank's forward + backward
+    # (~100 kernels for config C), then NCCL all-gathers of the outputs
+    # [B, R] and input gradients [B, K] into every rank's device buffers
+    sp = ShardedPass(tc, B_global, dt, _lib.KLAY_LOG, world, rank, device=dev)
+    B = sp.local_batch
+    w_host = w_all[sp.lo:sp.hi]
+    sp.weights.copy_(torch.from_numpy(w_host.astype(np.float32)))
+    plan = sp.plan
 
-    def step():
-        cap.replay()
-        if world > 1:
-            dist.all_gather(gathered, cap.outputs)
-
-    stream = torch.cuda.current_stream(dev)
     clocks = ClockSampler(local)
     clocks.start()
     for _ in range(max(args.warmup, 3)):
-        step()
+        sp.step()
+    torch.cuda.synchronize(dev)
+    # kernels per step: count one stream-launched step (a replay launches
+    # the same captured kernels)
+    cap = sp.cap
+    n_a = lib.klay_launch_count()
+    plan.forward(cap.weights, _lib.KLAY_LOG, dt, retain=True, values=cap.values,
+                 outputs=cap.outputs, workspace=cap._fw)
+    plan.backward(cap.values, B, _lib.KLAY_LOG, dt, grads=cap.grads, workspace=cap._bw)
+    launches_per_step = lib.klay_launch_count() - n_a
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    # kernels per step (a graph replay launches the captured kernels; count
-    # them on one stream-launched step)
-    n_a = lib.klay_launch_count()
-    plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
-    plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
-    launches_per_step = lib.klay_launch_count() - n_a
-    torch.cuda.synchronize(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream(dev)
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        sp.step()
     ev1.record(stream)
     torch.cuda.synchronize(dev)
-    launches = launches_per_step * args.steps
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -574,62 +812,69 @@ def run_gpu_arm(args):
         dist.barrier()
     clk = clocks.stop()
     ms_per_step = ms / args.steps
-    value = world * B / (ms_per_step / 1e3)
+    value = B_global / (ms_per_step / 1e3)
 
-    # ---- per-launch timing of one instrumented step (roofline) ----------
-    lib.klay_profiler_begin()
-    plan.forward(w_dev, _lib.KLAY_LOG, dt, retain=True, values=values, outputs=outputs)
-    plan.backward(values, B, _lib.KLAY_LOG, dt, grads=grads, workspace=work)
-    import ctypes
-    nslots = 4 * len(tc.layers) + 16
-    kinds = (ctypes.c_int32 * nslots)()
-    layers = (ctypes.c_int32 * nslots)()
-    tms = (ctypes.c_float * nslots)()
-    nrec = ctypes.c_int32()
-    lib.klay_profiler_end(nslots, kinds, layers, tms, ctypes.byref(nrec))
-    # the contract's figure and the bytes the implemented
-    # dataflow must move (unary-node aliases and routes skip rows)
-    fwd_b, bwd_b = survey_layer_bytes(tc, s, B)
-    fwd_n, bwd_n = layer_bytes(tc, s, B)
-    per_kind = {0: [0.0, 0.0, 0, 0.0], 1: [0.0, 0.0, 0, 0.0]}
-    other_ms = 0.0
-    for i in range(min(nrec.value, nslots)):
-        k, l, t = kinds[i], layers[i], tms[i]
-        if k in (0, 1):
-            per_kind[k][0] += t
-            per_kind[k][1] += (fwd_b if k == 0 else bwd_b)[l]
-            per_kind[k][2] += 1
-            per_kind[k][3] += (fwd_n if k == 0 else bwd_n)[l]
-        else:
-            other_ms += t
+    # ---- sustained: the same step replayed for >= args.sustain seconds ---
+    sustained = None
+    if args.sustain > 0:
+        n_sus = max(args.steps, int(args.sustain * 1e3 / ms_per_step) + 1)
+        cs = ClockSampler(local)
+        cs.start()
+        if world > 1:
+            dist.barrier()
+        ms_s = _timed_replays(sp.step, n_sus, dev) * n_sus
+        if world > 1:
+            t = torch.tensor([ms_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_s = float(t.item())
+        sustained = {"steps": n_sus, "seconds": ms_s / 1e3,
+                     "value": B_global * n_sus / (ms_s / 1e3), "ms_per_step": ms_s / n_sus,
+                     "clocks": cs.stop()}
+
+    # ---- per-template roofline: in-graph time of each launch class -------
+    def full_step():
+        plan.forward(cap.weights, _lib.KLAY_LOG, dt, retain=True, values=cap.values,
+                     outputs=cap.outputs, workspace=cap._fw)
+        plan.backward(cap.values, B, _lib.KLAY_LOG, dt, grads=cap.grads, workspace=cap._bw)
+
+    ctimes = time_classes(lib, full_step, iters=max(10, min(args.steps, 50)))
+    nec_b, sur_b, cls_layers = class_bytes(tc, plan, B, s)
     peak, peak_kind = load_peaks()
-    dom = max(per_kind, key=lambda k: per_kind[k][0])
-    dom_name = ["fwd_layer_kernel", "bwd_layer_kernel"][dom]
-    traffic = None
-    try:  # DRAM bytes of the same launches, from the committed ncu launch list
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(dom_name)
-    except Exception:
-        pass
-    dms, dbytes, dn, dnec = per_kind[dom]
-    achieved = dbytes / (dms / 1e3) / 1e9
-    achieved_nec = dnec / (dms / 1e3) / 1e9
+    ncu = ncu_class_traffic(os.path.join(ROOT, "profiles", args.launch_list))
+    templates = {}
+    for c, t in ctimes.items():
+        sec = t["ms"] / 1e3
+        row = {"launches": t["launches"], "layers": len(cls_layers[c]), "ms": t["ms"],
+               "necessary_bytes": nec_b[c], "contract_bytes": sur_b[c],
+               "achieved_gbs": nec_b[c] / sec / 1e9, "frac": nec_b[c] / sec / 1e9 / peak,
+               "contract_frac": sur_b[c] / sec / 1e9 / peak}
+        if ncu and c in ncu:
+            row["ncu_dram_bytes"] = ncu[c]["dram_bytes"]
+            row["ncu_ms"] = ncu[c]["ms"]
+            row["ncu_frac"] = (nec_b[c] / (ncu[c]["ms"] / 1e3) / 1e9 / peak
+                               if ncu[c]["ms"] else None)
+        templates[c] = row
+    dom = max(templates, key=lambda c: templates[c]["ms"])
+    dt_ = templates[dom]
+    nl = dt_["launches"]
     bpe = bytes_per_eval(tc, s, B, survey=True)
-    bpe_nec = bytes_per_eval(tc, s, B)
+    bpe_nec = sum(nec_b.values()) / B
 
     # ---- e2e: public API with host buffers ------------------------------
     e2e = None
     if not args.no_e2e:
-        W = engine.WeightAssignment(w_host, "log")
+        def api(rows):
+            return engine.gradient(tc, engine.WeightAssignment(rows, "log"), log_domain=True,
+                                   dtype=np.float32)
         for _ in range(2):
-            engine.gradient(tc, W, log_domain=True, dtype=np.float32)
+            sharded_eval(api, w_all, world, rank)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         n_e2e = max(3, min(args.steps, 20))
         for _ in range(n_e2e):
-            out, g = engine.gradient(tc, W, log_domain=True, dtype=np.float32)
+            out, g = sharded_eval(api, w_all, world, rank)
         torch.cuda.synchronize(dev)
         el = time.perf_counter() - t0
         engine.clear_cache()
@@ -637,15 +882,36 @@ def run_gpu_arm(args):
             t = torch.tensor([el], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": world * B * n_e2e / el, "unit": "evals/s",
+        e2e = {"value": B_global * n_e2e / el, "unit": "evals/s",
                "h2d_bytes_per_step": int(w_host.size * 4),
-               "d2h_bytes_per_step": int(out.nbytes + g.nbytes),
-               "api": "engine.gradient(log_domain=True, dtype=float32): numpy in/out; one "
-                      "CUDA graph per call holding the pinned H2D copy, fwd, bwd and D2H copies"}
+               "d2h_bytes_per_step": int(B * (tc.num_roots + tc.num_inputs) * 4),
+               "api": "engine.gradient(log_domain=True, dtype=float32) on this rank's rows: "
+                      "numpy in/out, one CUDA graph per call holding the pinned H2D copy, fwd, "
+                      "bwd and D2H copies" + ("; outputs + grads all-gathered "
+                                              "(distributed.sharded_eval)" if world > 1 else "")}
+
+    # ---- weak scaling (N > 1): 1024 rows per rank ------------------------
+    weak = None
+    if world > 1 and strong and not args.no_weak:
+        wp = ShardedPass(tc, args.batch * world, dt, _lib.KLAY_LOG, world, rank, device=dev)
+        rng2 = np.random.Generator(np.random.Philox(key=2))
+        wp.weights.copy_(torch.from_numpy(np.log(rng2.uniform(
+            0.05, 0.95, size=(wp.local_batch, tc.num_inputs))).astype(np.float32)))
+        for _ in range(3):
+            wp.step()
+        dist.barrier()
+        ms_w = _timed_replays(wp.step, args.steps, dev)
+        t = torch.tensor([ms_w], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_w = float(t.item())
+        weak = {"rows_per_gpu": args.batch, "global_batch": args.batch * world,
+                "ms_per_step": ms_w, "value": args.batch * world / (ms_w / 1e3)}
 
     extra = None
     if world == 1 and not args.no_extra:
-        # the other BASELINE configs, device-timed (parity cases; not the headline)
+        # the other BASELINE configs and a 1-GPU batch sweep of config C (the
+        # strong-scaling proxy: 1024 / G rows per GPU at G = 2, 4, 8),
+        # device-timed; parity cases, not the headline
         extra = {
             "A_real_f64_b1_fwd": measure_config("A", "real", np.float64, 1, False, dev),
             "B_log_f64_b256_fwd_bwd": measure_config("B", "log", np.float64, 256, True, dev),
@@ -654,8 +920,13 @@ def run_gpu_arm(args):
             "D_bool_packed_b4096_fwd": measure_config("D", "bool_packed", "u1", 4096, False, dev),
             "D_real_f32_b4096_fwd": measure_config("D", "real", np.float32, 4096, False, dev),
             "E_log_f64_b128_fwd_bwd": measure_config("E", "log", np.float64, 128, True, dev),
-            "Cp_log_f32_b1024_fwd_bwd": measure_config("Cp", "log", np.float32, 1024, True, dev, iters=5),
+            "Cp_log_f32_b1024_fwd_bwd": measure_config("Cp", "log", np.float32, 1024, True, dev,
+                                                       iters=5),
         }
+        for b in (512, 256, 128):
+            r = measure_config("C", "log", np.float32, b, True, dev)
+            r["linear_share_ratio"] = r["ms_per_batch"] / (ms_per_step * b / B_global)
+            extra[f"C_log_f32_b{b}_fwd_bwd"] = r
 
     if world > 1:
         dist.barrier()
@@ -666,43 +937,47 @@ def run_gpu_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "nodes": nodes,
                    "edges": int(sum(len(l.sources) for l in tc.layers)),
                    "gate_layers": len(tc.layers), "semiring": "log", "pass": "fwd+bwd",
-                   "batch_per_gpu": B, "global_batch": B * world,
-                   "parallelism": f"dp{world} (batch-sharded, plan replicated)",
+                   "global_batch": B_global, "batch_per_gpu": B,
+                   "parallelism": f"dp{world} (batch-sharded, plan replicated; NCCL all-gather "
+                                  "of outputs and grads each step)",
                    "l2": f"no flush: per-step working set {nodes * B * s / 1e9:.2f} GB trace "
                          ">> 126 MB L2",
-                   "bytes_per_eval": bpe,
-                   "bytes_model": "SURVEY §8(d) (reference dataflow: every layer read and "
-                                  "written, c_l = 2 for log-sum layers)",
-                   "step_roofline_frac": value / world * bpe / (peak * 1e9),
                    "bytes_per_eval_necessary": bpe_nec,
                    "step_frac_necessary": value / world * bpe_nec / (peak * 1e9),
-                   "necessary_model": "bytes the implemented dataflow must move: unary-node "
-                                      "aliases and adjoint routes skip rows (bench.py "
-                                      "layer_bytes / alias_plan)"},
-        "roofline": {"bound": "hbm", "kernel": dom_name,
-                     "launches_per_step": dn, "achieved": achieved, "peak": peak,
-                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "alg_bytes_per_step": dbytes,
-                     "alg_model": "SURVEY §8(d) per-layer bytes x launches",
-                     "necessary": {"alg_bytes_per_step": dnec, "achieved": achieved_nec,
-                                   "frac": achieved_nec / peak},
-                     "traffic": traffic,
-                     "traffic_scope": "DRAM read+write bytes per step of the same launches "
-                                      "(ncu launch list, profiles/traffic.json)",
-                     "kernel_ms_per_step": dms,
-                     "fwd_ms": per_kind[0][0], "bwd_ms": per_kind[1][0],
-                     "boundary_ms": other_ms},
-        "gpu_launches": int(launches),
+                   "necessary_model": "bytes the implemented dataflow must move per launch "
+                                      "class (bench.py class_bytes: layer_bytes for layer "
+                                      "kernels, unary-node aliases and routes skip rows)",
+                   "bytes_per_eval_contract": bpe,
+                   "step_contract_frac": value / world * bpe / (peak * 1e9),
+                   "contract_model": "SURVEY §8(d) (reference dataflow: every layer read and "
+                                     "written, c_l = 2 for log-sum layers)"},
+        "roofline": {"bound": "hbm", "kernel": dom,
+                     "achieved": dt_["achieved_gbs"], "peak": peak, "peak_source": peak_kind,
+                     "unit": "GB/s", "frac": dt_["frac"],
+                     "contract_frac": dt_["contract_frac"],
+                     "traffic": (dt_["ncu_dram_bytes"] / nl) if "ncu_dram_bytes" in dt_ else None,
+                     "traffic_scope": f"ncu DRAM read+write bytes per launch of the dominant "
+                                      f"class (profiles/{args.launch_list}, same build and "
+                                      "workload)",
+                     "bytes_per_launch": dt_["necessary_bytes"] / nl,
+                     "launches_per_step": nl, "ms_per_step": dt_["ms"],
+                     "timing": "in-graph: one CUDA graph of just this class's launches of a "
+                               "step, replayed between CUDA events (bench.py time_classes)",
+                     "templates": templates,
+                     "sum_template_ms": sum(t["ms"] for t in templates.values())},
+        "gpu_launches": int(launches_per_step * args.steps),
         "launch_mode": "CUDA graph replay of the captured fwd+bwd "
                        f"({launches_per_step} libklay kernels per step)",
         "clocks": clk,
+        "sustained": sustained,
         "cpu_baseline": cpu_line,
         "e2e": e2e,
+        "weak_scaling": weak,
         "extra_configs": extra,
     }
     print(json.dumps(line), flush=True)
@@ -715,14 +990,23 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=1024, help="rows per GPU")
+    ap.add_argument("--batch", type=int, default=1024,
+                    help="global batch (strong scaling) or rows per GPU (weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--sustain", type=float, default=2.0, help="seconds of sustained replay")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-single-seconds", type=float, default=4.0)
+    ap.add_argument("--launch-list", default="r2_launches.csv",
+                    help="committed ncu launch list under profiles/ (per-class DRAM bytes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other-config measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_gpu_arm(args)
 
 

@@ -229,6 +229,22 @@ KLAY_API int klay_profiler_begin(void);
 KLAY_API int klay_profiler_end(int32_t max_records, int32_t* kinds, int32_t* layers, float* ms,
                       int32_t* n_records);
 
+/* Launch classes (per-template roofline accounting in bench.py). */
+#define KLAY_CLASS_FWD_PROD 0     /* forward layer kernel, product layer        */
+#define KLAY_CLASS_FWD_SUM 1      /* forward layer kernel, sum layer            */
+#define KLAY_CLASS_BWD_PASS 2     /* backward pass-through (incl. route masks)  */
+#define KLAY_CLASS_BWD_LOGSUM 3   /* backward log-sum (softmax edge weights)    */
+#define KLAY_CLASS_BWD_REALPROD 4 /* backward real product (zero-safe adjoint)  */
+#define KLAY_CLASS_FWD_MICRO 5    /* forward micro tail / micro head            */
+#define KLAY_CLASS_BWD_MICRO 6    /* backward micro tail / micro head           */
+#define KLAY_CLASS_TAIL 7         /* persistent cluster tail (either direction) */
+#define KLAY_CLASS_BOUNDARY 8     /* inputs, outputs, seeds, grads              */
+/* Profiling hook: launch only the kernels whose class bit is set in
+ * `class_mask` on this thread (default all); returns the previous mask.
+ * A pass captured with a filter holds just those launches, so it times one
+ * template inside a CUDA graph. Results of a filtered pass are garbage. */
+KLAY_API uint32_t klay_set_launch_filter(uint32_t class_mask);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,7 @@ SIGNATURES = {
     "klay_layered_destroy": (None, [_vp]),
     "klay_layerize_error": (ctypes.c_char_p, []),
     "klay_launch_count": (_c_i64, []),
+    "klay_set_launch_filter": (ctypes.c_uint32, [ctypes.c_uint32]),
     "klay_profiler_begin": (ctypes.c_int, []),
     "klay_profiler_end": (ctypes.c_int, [_c_i32, _vp, _vp, _vp, _vp]),
 }

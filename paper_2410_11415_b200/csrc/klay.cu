@@ -151,6 +151,11 @@ int fail(int code, const std::string& msg) {
 // Kernel launches issued by this library (all threads).
 std::atomic<long long> g_launches{0};
 
+// Launch-class filter (klay_set_launch_filter; profiling only): bit c set =
+// kernels of class KLAY_CLASS_* c are launched. Per thread, default all.
+thread_local uint32_t g_launch_filter = 0xffffffffu;
+inline bool launch_on(int cls) { return (g_launch_filter >> cls) & 1u; }
+
 // Optional per-launch event timing (klay_profiler_begin / _end).
 struct ProfRec {
   int kind, layer;
@@ -1013,7 +1018,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* pingpong[2] = {values, values + (size_t)p->max_width * ld};
   constexpr bool U1 = std::is_same<T, unsigned>::value;
-  if (p->K > 0) {
+  if (p->K > 0 && launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 2, 0);
     if constexpr (U1) {
       launch_pack_inputs(weights, wdt == KLAY_F64, values, (int)p->K, B, ld, nullptr, s);
@@ -1048,6 +1053,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     m.V = V;
     m.ld = ld;
     m.eps = (T)eps;
+    if (!launch_on(KLAY_CLASS_FWD_MICRO)) return KLAY_OK;
     LaunchScope ls(s, 6, first + 1);
     int n;
     if constexpr (U1) n = launch_forward_micro_u1(m, s);
@@ -1132,13 +1138,17 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       micro.prod[i] = d.prod ? 1 : 0;
     } else if (l >= tail_from) {
       tail->layer[tail->n++] = a;
-    } else {
+    } else if (launch_on(d.prod ? KLAY_CLASS_FWD_PROD : KLAY_CLASS_FWD_SUM)) {
       a.hcount = hcount;
       LaunchScope ls(s, 0, l + 1);
       if constexpr (U1) g_launches += launch_forward_layer_u1(d.prod, a, s);
       else g_launches += launch_forward_layer(sr, d.prod, redo, a, s);
     }
     prev = cur;
+  }
+  if (tail && !launch_on(KLAY_CLASS_TAIL)) {
+    delete tail;
+    tail = nullptr;
   }
   if (tail) {
     const LayerDesc& d0 = p->layers[tail_from];
@@ -1171,7 +1181,7 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     const int rc = run_micro(micro, micro_from);
     if (rc != KLAY_OK) return rc;
   }
-  if (outputs && p->R > 0) {
+  if (outputs && p->R > 0 && launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 2, p->L + 1);
     if constexpr (U1) {
       launch_unpack_outputs(prev, p->d_root_node, p->d_const, outputs, wdt == KLAY_F64, p->R, B, ld, s);
@@ -1200,7 +1210,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     const size_t nb = counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld);
     KLAY_CUDA(cudaMemsetAsync(hcount, 0, nb, s));
   }
-  {
+  if (launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 3, p->L + 1);
     launch_seed<T>(seed, p->d_top_off, p->d_top_pos, gtrace + (size_t)p->layer_row[p->L] * ld,
                    (int)p->WL, p->R, B, ld, s);
@@ -1253,7 +1263,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       m.csr_n[i] = (domain == SR_LOG_ ? p->microb_n : p->microbr_n)[l];
       // weighted layers: log sums (softmax weights), real products (zero-safe)
       m.logsum[i] = (domain == SR_LOG_) ? (d.prod ? 0 : 1) : (d.prod ? 1 : 0);
-      if (l == lowest) {
+      if (l == lowest && launch_on(KLAY_CLASS_BWD_MICRO)) {
         m.csr = p->d_microb;
         m.V = V;
         m.ld = ld;
@@ -1269,7 +1279,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       }
     } else if (l >= tail_from) {
       tail->layer[tail->n++] = a;
-      if (l == tail_from) {
+      if (l == tail_from && !launch_on(KLAY_CLASS_TAIL)) {
+        delete tail;
+        tail = nullptr;
+      } else if (l == tail_from) {
         const LayerDesc& d0 = p->layers[tail_from];
         const LayerDesc& dl = p->layers[microb_from - 1];
         tail->pf_ptr[0] = p->d_tpar + d0.e_base;
@@ -1309,11 +1322,15 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
         a.nprev = trace;
         if (d.bmask) mode = BW_PASSA_;
       }
-      LaunchScope ls(s, 1, l + 1);
-      g_launches += launch_backward_layer(mode, a, s);
+      const int cls = (mode == BW_PASS_ || mode == BW_PASSA_) ? KLAY_CLASS_BWD_PASS
+                      : (mode == BW_REALPROD_ ? KLAY_CLASS_BWD_REALPROD : KLAY_CLASS_BWD_LOGSUM);
+      if (launch_on(cls)) {
+        LaunchScope ls(s, 1, l + 1);
+        g_launches += launch_backward_layer(mode, a, s);
+      }
     }
   }
-  if (p->K > 0) {
+  if (p->K > 0 && launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 3, 0);
     launch_store_rows<T>(gtrace, grads, (int)p->K, B, ld, s);
     ++g_launches;
@@ -1396,6 +1413,12 @@ extern "C" int klay_fill_trace(const KlayPlan* plan, int32_t semiring, int32_t d
 }
 
 extern "C" int64_t klay_launch_count(void) { return g_launches.load(); }
+
+extern "C" uint32_t klay_set_launch_filter(uint32_t class_mask) {
+  const uint32_t prev = g_launch_filter;
+  g_launch_filter = class_mask;
+  return prev;
+}
 
 extern "C" int klay_profiler_begin(void) {
   for (auto& r : g_prof) {

@@ -17,6 +17,8 @@ the torch module and the benchmark (inputs already in HBM).
 from __future__ import annotations
 
 import ctypes
+import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import Mapping, Sequence
 
@@ -270,6 +272,31 @@ class DevicePlan:
             return None
         return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
 
+    # ---- caller-buffer validation (the C ABI sees raw pointers only) -------
+    def _check_buf(self, t, name, dtype, shape=None, min_rows=None, min_bytes=None):
+        """Raise EvalError unless `t` is a contiguous tensor of `dtype` on this
+        plan's device with the given exact `shape`, at least `min_rows` rows
+        or at least `min_bytes` bytes."""
+        if t.device != self.device:
+            raise EvalError(f"{name} is on {t.device}, the circuit plan on {self.device}")
+        if dtype is not None and t.dtype != dtype:
+            raise EvalError(f"{name} has dtype {t.dtype}, expected {dtype}")
+        if not t.is_contiguous():
+            raise EvalError(f"{name} must be contiguous")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise EvalError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        if min_rows is not None and (t.dim() != 2 or t.shape[0] < min_rows):
+            raise EvalError(f"{name} has {t.shape[0] if t.dim() else 0} rows, needs >= {min_rows}")
+        if min_bytes is not None and t.numel() * t.element_size() < min_bytes:
+            raise EvalError(f"{name} has {t.numel() * t.element_size()} bytes, needs >= {min_bytes}")
+
+    def _check_values(self, values, batch, dtype, retain):
+        ld = self.row_stride(batch, dtype)
+        rows = self.num_nodes if retain else 2 * self.max_width
+        self._check_buf(values, "values", _torch_dtype(dtype), min_rows=rows)
+        if values.shape[1] < ld:
+            raise EvalError(f"values rows hold {values.shape[1]} elements, batch {batch} needs {ld}")
+
     def forward(self, weights, semiring: int, dtype, retain=True, epsilon=0.0,
                 values=None, outputs=None, workspace=None):
         """weights: cuda tensor [B, K] (float32/float64, semiring domain).
@@ -283,20 +310,29 @@ class DevicePlan:
         B = int(weights.shape[0])
         if B < 1:
             raise EvalError("batch must be >= 1")
+        if weights.dtype not in (torch.float32, torch.float64):
+            raise EvalError("weights must be float32 or float64")
+        if weights.device != self.device:
+            raise EvalError(f"weights are on {weights.device}, the circuit plan on {self.device}")
         if not weights.is_contiguous():
             weights = weights.contiguous()
         wdt = _lib.KLAY_F64 if weights.dtype == torch.float64 else _lib.KLAY_F32
-        if weights.dtype not in (torch.float32, torch.float64):
-            raise EvalError("weights must be float32 or float64")
         if values is None:
             values = self.alloc_values(B, dtype, retain)
+        else:
+            self._check_values(values, B, dtype, retain)
         ld = values.shape[1]
         # bit-packed Boolean rows return 0/1 outputs in the weights' dtype
         tdt = weights.dtype if _klay_dtype(dtype) == _lib.KLAY_U1 else _torch_dtype(dtype)
         if outputs is None:
             outputs = torch.empty((B, self.num_roots), dtype=tdt, device=self.device)
+        else:
+            self._check_buf(outputs, "outputs", tdt, shape=(B, self.num_roots))
+        need = int(self._lib.klay_forward_workspace(self._handle, _klay_dtype(dtype), ld))
         if workspace is None:
-            workspace = self.forward_workspace(B, dtype)
+            workspace = torch.empty(need, dtype=torch.uint8, device=self.device) if need else None
+        elif need:
+            self._check_buf(workspace, "workspace", None, min_bytes=need)
         mode = 0 if not retain else (1 if retain == "full" else _lib.KLAY_RETAIN_BACKWARD)
         rc = self._lib.klay_forward(
             self._handle, semiring, _klay_dtype(dtype), weights.data_ptr(), wdt,
@@ -344,11 +380,22 @@ class DevicePlan:
         recorded on `values`; unknown disables the unary-parent shortcut).
         Returns grads [B, K] tensor."""
         torch = _torch()
+        if isinstance(dtype, str) and dtype == U1:
+            raise EvalError("no backward for bit-packed Boolean rows")
         tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        if batch < 1:
+            raise EvalError("batch must be >= 1")
+        self._check_values(values, batch, dtype, True)
+        ld = values.shape[1]
         if grads is None:
             grads = torch.empty((batch, self.num_inputs), dtype=tdt, device=self.device)
+        else:
+            self._check_buf(grads, "grads", tdt, shape=(batch, self.num_inputs))
+        need = int(self._lib.klay_backward_workspace(self._handle, _klay_dtype(dtype), ld))
         if workspace is None:
-            workspace = self.workspace(batch, dtype)
+            workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
+        else:
+            self._check_buf(workspace, "workspace", None, min_bytes=need)
         if seed is not None:
             if tuple(seed.shape) != (batch, self.num_roots):
                 raise EvalError(f"seed must have shape {(batch, self.num_roots)}")
@@ -542,6 +589,26 @@ def forward_log(tc, weights: WeightAssignment, epsilon: float = 0.0, retain_trac
     return EvalTrace(LOG_DOMAIN, out, nv, epsilon, buf if retain_trace else None, plan, dt)
 
 
+def _device_semiring(semiring) -> Semiring:
+    """The device semiring for ``semiring``: one of this module's instances,
+    or any object with the reference ``Semiring`` fields (engine.py:158-191)
+    whose name and identities are those of a built-in one -- e.g. the
+    reference's own REAL / BOOLEAN / MAX_PRODUCT. Semirings with other
+    reductions have no device kernels and raise (there is no CPU path)."""
+    if isinstance(semiring, Semiring) and SEMIRINGS.get(semiring.name) is semiring:
+        return semiring
+    name = getattr(semiring, "name", None)
+    ours = SEMIRINGS.get(name) if isinstance(name, str) else None
+    if ours is None:
+        raise EvalError(f"unsupported semiring {name if name is not None else semiring!r}: only "
+                        f"{sorted(SEMIRINGS)} and 'log' have device kernels")
+    if (float(getattr(semiring, "zero", ours.zero)) != ours.zero
+            or float(getattr(semiring, "one", ours.one)) != ours.one):
+        raise EvalError(f"semiring {name!r} has identities ({semiring.zero}, {semiring.one}); "
+                        f"the device {name!r} semiring uses ({ours.zero}, {ours.one})")
+    return ours
+
+
 def evaluate_semiring(tc, weights: WeightAssignment, semiring) -> np.ndarray:
     """Forward evaluation under a named semiring; returns [batch, roots]."""
     if isinstance(semiring, str):
@@ -550,8 +617,7 @@ def evaluate_semiring(tc, weights: WeightAssignment, semiring) -> np.ndarray:
         if semiring not in SEMIRINGS:
             raise EvalError(f"unknown semiring {semiring!r}")
         semiring = SEMIRINGS[semiring]
-    if not isinstance(semiring, Semiring) or semiring.name not in SEMIRINGS:
-        raise EvalError(f"unsupported semiring {getattr(semiring, 'name', semiring)!r}")
+    semiring = _device_semiring(semiring)
     _check_shapes(tc, weights)
     dt = np.float64
     if semiring is BOOLEAN and np.all((weights.values == 0.0) | (weights.values == 1.0)):
@@ -605,23 +671,55 @@ def backward(tc, trace: EvalTrace, seed: np.ndarray | None = None) -> np.ndarray
     return grads.cpu().numpy()
 
 
-_PASS_CACHE: dict = {}
+# gradient()'s captured passes: at most ONE per device plan, stored on the
+# plan itself (so it dies with the circuit) and replaced when the batch,
+# dtype, domain, epsilon or seeding changes. A per-plan lock makes the
+# write-inputs / replay / read-outputs sequence atomic: concurrent callers on
+# one circuit serialize instead of sharing the pinned buffers.
+_PLANS_WITH_PASS: "weakref.WeakSet" = None  # filled lazily (clear_cache)
+_PASS_LOCK = threading.Lock()               # guards creation of per-plan locks
+
+
+def _plan_pass_lock(plan) -> threading.Lock:
+    lock = getattr(plan, "_grad_lock", None)
+    if lock is None:
+        with _PASS_LOCK:
+            lock = getattr(plan, "_grad_lock", None)
+            if lock is None:
+                lock = plan._grad_lock = threading.Lock()
+    return lock
 
 
 def clear_cache() -> None:
     """Drop the cached captured passes of ``gradient`` (frees their buffers)."""
-    _PASS_CACHE.clear()
+    global _PLANS_WITH_PASS
+    if _PLANS_WITH_PASS is None:
+        return
+    for plan in list(_PLANS_WITH_PASS):
+        with _plan_pass_lock(plan):
+            plan._grad_pass = None
+    _PLANS_WITH_PASS.clear()
+
+
+def cached_passes() -> int:
+    """Number of captured ``gradient`` passes currently resident."""
+    if _PLANS_WITH_PASS is None:
+        return 0
+    return sum(1 for p in list(_PLANS_WITH_PASS) if getattr(p, "_grad_pass", None) is not None)
 
 
 def gradient(tc, weights: WeightAssignment, log_domain: bool = False, epsilon: float = 0.0,
              seed: np.ndarray | None = None, dtype=None) -> tuple[np.ndarray, np.ndarray]:
     """Forward + backward; returns (outputs, input grads) (engine.py:372-384).
 
-    No trace escapes this call, so it runs a CUDA-graph-captured pass cached
-    per (circuit, batch, dtype, domain, epsilon, seeded): one H2D copy of the
-    weights (and seed), one graph replay, one D2H copy of outputs and grads.
-    ``dtype`` (float64 default, or float32) is an extension of the reference
-    signature; ``clear_cache()`` frees the cached buffers."""
+    No trace escapes this call, so it runs a CUDA-graph-captured pass: one
+    H2D copy of the weights (and seed), one graph replay, one D2H copy of
+    outputs and grads. One pass is cached per circuit (replaced when the
+    batch, dtype, domain, epsilon or seeding changes); calls on one circuit
+    from several threads serialize on a per-circuit lock. ``dtype`` (float64
+    default, or float32) is an extension of the reference signature;
+    ``clear_cache()`` frees the cached buffers."""
+    global _PLANS_WITH_PASS
     torch = _torch()
     w = weights.to_log() if log_domain else weights
     if log_domain and epsilon < 0:
@@ -635,21 +733,28 @@ def gradient(tc, weights: WeightAssignment, log_domain: bool = False, epsilon: f
     plan = device_plan(tc)
     B = w.batch
     code = _lib.KLAY_LOG if log_domain else _lib.KLAY_REAL
-    key = (id(plan), B, np.dtype(dt).str, code, float(epsilon), seed is not None)
-    cap = _PASS_CACHE.get(key)
-    if cap is None or cap.plan is not plan:
-        cap = plan.capture(B, dt, code, epsilon=epsilon, backward=True, seeded=seed is not None,
-                           host_io=True)
-        _PASS_CACHE[key] = cap
     if seed is not None:
         sd = np.asarray(seed, dtype=np.dtype(dt))
         if sd.shape != (B, tc.num_roots):
             raise EvalError(f"seed must have shape {(B, tc.num_roots)}")
-    # (pinned buffers idle: the previous call synchronized; torch's copy_
-    # converts on several host threads)
-    cap.h_weights.copy_(torch.from_numpy(np.ascontiguousarray(w.values)))
-    if seed is not None:
-        cap.h_seed.copy_(torch.from_numpy(np.ascontiguousarray(sd)))
-    cap.replay()  # H2D, forward, backward, D2H: one graph launch
-    torch.cuda.current_stream(plan.device).synchronize()
-    return cap.h_out.clone().numpy(), cap.h_grad.clone().numpy()
+    key = (B, np.dtype(dt).str, code, float(epsilon), seed is not None)
+    with _plan_pass_lock(plan):
+        entry = getattr(plan, "_grad_pass", None)
+        if entry is None or entry[0] != key:
+            plan._grad_pass = None  # free the old buffers before allocating new ones
+            cap = plan.capture(B, dt, code, epsilon=epsilon, backward=True,
+                               seeded=seed is not None, host_io=True)
+            plan._grad_pass = (key, cap)
+            with _PASS_LOCK:
+                if _PLANS_WITH_PASS is None:
+                    _PLANS_WITH_PASS = weakref.WeakSet()
+                _PLANS_WITH_PASS.add(plan)
+        cap = plan._grad_pass[1]
+        # (pinned buffers idle: the previous call synchronized; torch's copy_
+        # converts on several host threads)
+        cap.h_weights.copy_(torch.from_numpy(np.ascontiguousarray(w.values)))
+        if seed is not None:
+            cap.h_seed.copy_(torch.from_numpy(np.ascontiguousarray(sd)))
+        cap.replay()  # H2D, forward, backward, D2H: one graph launch
+        torch.cuda.current_stream(plan.device).synchronize()
+        return cap.h_out.clone().numpy(), cap.h_grad.clone().numpy()

@@ -71,3 +71,43 @@ def test_two_rank_gloo_sharding_matches_single_process(tmp_path, name):
     for r in range(world):
         assert np.array_equal(np.load(tmp_path / f"out{r}.npy"), out)
         assert np.array_equal(np.load(tmp_path / f"grad{r}.npy"), grad)
+
+
+def _gather_worker(rank, world, port, result_dir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_11415_b200.distributed import gather_rows, shard_bounds
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B = 11
+        sizes = [b - a for a, b in (shard_bounds(B, world, r) for r in range(world))]
+        lo, hi = shard_bounds(B, world, rank)
+        full = torch.arange(B * 3, dtype=torch.float64).reshape(B, 3)
+        out = torch.full((B, 3), -1.0, dtype=torch.float64)
+        got = gather_rows(full[lo:hi], world, sizes=sizes, out=out)
+        assert got is out
+        assert torch.equal(out, full)
+        got2 = gather_rows(full[lo:hi].clone(), world)  # counts exchanged
+        assert torch.equal(got2, full)
+        try:
+            gather_rows(full[lo:hi], world, sizes=[B, 0, 0][:world])
+            bad = False
+        except ValueError:
+            bad = True
+        np.save(os.path.join(result_dir, f"ok{rank}.npy"), np.array([bad]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gather_rows_uneven_into_out(tmp_path):
+    """gather_rows with precomputed shard sizes (bench.py / ShardedPass) and
+    a preallocated output, uneven shards (6 + 5 rows), and a size mismatch
+    raising ValueError on the rank whose count disagrees."""
+    world = 2
+    mp.start_processes(_gather_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    assert bool(np.load(tmp_path / "ok1.npy")[0])
