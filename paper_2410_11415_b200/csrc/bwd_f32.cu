@@ -1,5 +1,6 @@
 // Backward layer kernels for float (explicit instantiations).
 #include "layer_kernels.cuh"
+#include "stream_kernels.cuh"
 
 namespace klay {
 
@@ -10,6 +11,16 @@ int launch_backward_layer(int mode, const LayerArgs<float>& a, cudaStream_t s) {
     case BW_REALPROD: return launch_layer<float, RK_SUM, BwdGather<float, BW_REALPROD>>(a, s);
     case BW_PASSA: return launch_layer<float, RK_SUM, BwdGather<float, BW_PASSA>>(a, s);
     default: return launch_layer<float, RK_SUM, BwdGather<float, BW_PASS>>(a, s);
+  }
+}
+
+int launch_backward_stream(int mode, const LayerArgs<float>& a, cudaStream_t s) {
+  switch (mode) {
+    case BW_LOGSUM:
+    case BW_LOGSUM8: return launch_stream<float, RK_SUM, BwdGather<float, BW_LOGSUM>>(a, s);
+    case BW_REALPROD: return launch_stream<float, RK_SUM, BwdGather<float, BW_REALPROD>>(a, s);
+    case BW_PASSA: return launch_stream<float, RK_SUM, BwdGather<float, BW_PASSA>>(a, s);
+    default: return launch_stream<float, RK_SUM, BwdGather<float, BW_PASS>>(a, s);
   }
 }
 

@@ -1,5 +1,6 @@
 // Forward layer kernels for float (explicit instantiations).
 #include "layer_kernels.cuh"
+#include "stream_kernels.cuh"
 
 namespace klay {
 
@@ -20,6 +21,25 @@ int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<float>& 
     default:  // max-product
       if (prod) return launch_layer<float, RK_PROD, G>(a, s);
       else return launch_layer<float, RK_MAX, G>(a, s);
+  }
+}
+
+int launch_forward_stream(int sr, bool prod, bool alias, const LayerArgs<float>& a, cudaStream_t s) {
+  using G = FwdGather<float>;
+  if (alias) return launch_stream<float, RK_SUM, FwdGather<float, true>>(a, s);
+  switch (sr) {
+    case SR_REAL:
+      if (prod) return launch_stream<float, RK_PROD, G>(a, s);
+      else return launch_stream<float, RK_SUM, G>(a, s);
+    case SR_LOG:
+      if (prod) return launch_stream<float, RK_SUM, G>(a, s);
+      else return launch_stream<float, RK_LSE, G>(a, s);
+    case SR_BOOL:
+      if (prod) return launch_stream<float, RK_MIN, G>(a, s);
+      else return launch_stream<float, RK_MAX, G>(a, s);
+    default:  // max-product
+      if (prod) return launch_stream<float, RK_PROD, G>(a, s);
+      else return launch_stream<float, RK_MAX, G>(a, s);
   }
 }
 

@@ -1,5 +1,6 @@
 // Forward layer kernels for double (explicit instantiations).
 #include "layer_kernels.cuh"
+#include "stream_kernels.cuh"
 
 namespace klay {
 
@@ -20,6 +21,25 @@ int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<double>&
     default:  // max-product
       if (prod) return launch_layer<double, RK_PROD, G>(a, s);
       else return launch_layer<double, RK_MAX, G>(a, s);
+  }
+}
+
+int launch_forward_stream(int sr, bool prod, bool alias, const LayerArgs<double>& a, cudaStream_t s) {
+  using G = FwdGather<double>;
+  if (alias) return launch_stream<double, RK_SUM, FwdGather<double, true>>(a, s);
+  switch (sr) {
+    case SR_REAL:
+      if (prod) return launch_stream<double, RK_PROD, G>(a, s);
+      else return launch_stream<double, RK_SUM, G>(a, s);
+    case SR_LOG:
+      if (prod) return launch_stream<double, RK_SUM, G>(a, s);
+      else return launch_stream<double, RK_LSE, G>(a, s);
+    case SR_BOOL:
+      if (prod) return launch_stream<double, RK_MIN, G>(a, s);
+      else return launch_stream<double, RK_MAX, G>(a, s);
+    default:  // max-product
+      if (prod) return launch_stream<double, RK_PROD, G>(a, s);
+      else return launch_stream<double, RK_MAX, G>(a, s);
   }
 }
 

@@ -129,6 +129,61 @@ const bool g_no_head = [] {
   return e && *e && *e != '0';
 }();
 
+// KLAY_STREAM=1: eligible layers on the bulk-copy streaming kernel
+// (stream_kernels.cuh) instead of items_kernel. Off by default: measured
+// slower on config C (DESIGN.md §4 "Streaming kernel"); kept, parity-tested,
+// for A/B runs.
+const bool g_no_stream = [] {
+  const char* e = getenv("KLAY_STREAM");
+  return !(e && *e && *e != '0');
+}();
+
+#ifdef KLAY_STREAM_TRACE
+// debug builds (-DKLAY_STREAM_TRACE): per-CTA timing of one streaming launch,
+// KLAY_STREAM_TRACE_LAYER = 1-based gate layer, KLAY_STREAM_TRACE_DIR = 0
+// forward / 1 backward; a summary goes to stderr after the launch
+void stream_trace_dump(unsigned long long* d, int n, int layer, int dir) {
+  std::vector<unsigned long long> h((size_t)8 * n);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull, t1 = 0;
+  double wait_gdc = 0, pw = 0, cw = 0, life = 0, plife = 0;
+  for (int i = 0; i < n; ++i) {
+    const unsigned long long* r = &h[(size_t)8 * i];
+    t0 = std::min(t0, r[0]);
+    t1 = std::max(t1, r[6]);
+    wait_gdc += (double)(r[1] - r[0]);
+    pw += (double)r[2];
+    cw += (double)r[5];
+    life += (double)(r[6] - r[1]);
+    plife += (double)(r[4] - r[1]);
+  }
+  fprintf(stderr,
+          "stream trace layer %d dir %d: %d CTAs, span %.1f us; per CTA mean: gdc wait %.2f us, "
+          "life %.2f us (producer %.2f us), producer empty-wait %.0f cyc, consumer full-wait %.0f cyc\n",
+          layer, dir, n, (t1 - t0) * 1e-3, wait_gdc / n * 1e-3, life / n * 1e-3, plife / n * 1e-3, pw / n,
+          cw / n);
+  FILE* f = fopen("stream_trace.bin", "wb");
+  if (f) {
+    fwrite(h.data(), 8, h.size(), f);
+    fclose(f);
+  }
+}
+unsigned long long* stream_trace_buf() {
+  static unsigned long long* b = nullptr;
+  if (!b) cudaMalloc(&b, (size_t)8 * 8 * 148 * 16 * 8);
+  return b;
+}
+const int g_trace_layer = [] {
+  const char* e = getenv("KLAY_STREAM_TRACE_LAYER");
+  return (e && *e) ? atoi(e) : -1;
+}();
+const int g_trace_dir = [] {
+  const char* e = getenv("KLAY_STREAM_TRACE_DIR");
+  return (e && *e) ? atoi(e) : 0;
+}();
+#endif
+
 const bool g_no_alias = [] {
   const char* e = getenv("KLAY_NO_ALIAS");
   return e && *e && *e != '0';
@@ -292,11 +347,57 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
   s.masks.insert(s.masks.end(), short_masks.begin(), short_masks.end());
 }
 
+// Streaming-kernel CTAs over the n nodes of a CSR (offsets o[base..base+n]):
+// contiguous node ranges {first node, end node, first edge, end edge}
+// balanced by slots (edges x slots per edge + two per node), about
+// STREAM_SPC slots per CTA, at most STREAM_MAXC CTAs, each CTA's index block
+// (3 ints per node + 1 per edge + 1) within STREAM_SIDX ints. The set is not
+// eligible (count 0) when a segment exceeds one numpy pairwise block
+// (MICRO_FAN edges): those layers keep items_kernel's heavy leaves.
+const int STREAM_SPC = [] {
+  const char* e = getenv("KLAY_STREAM_SPC");
+  return (e && *e) ? std::max(4, atoi(e)) : 256;
+}();
+constexpr int STREAM_MAXC = 148 * 16;
+constexpr int STREAM_SIDX_H = 2048;  // == klay::STREAM_SIDX
+void build_stream_ctas(const std::vector<int>& o, size_t base, int64_t n, int per_edge, std::vector<int4>& out,
+                       int64_t& at, int64_t& count) {
+  at = (int64_t)out.size();
+  count = 0;
+  if (n <= 0) return;
+  int64_t total = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int len = o[base + i + 1] - o[base + i];
+    if (len > MICRO_FAN) return;
+    total += (int64_t)len * per_edge + 2;
+  }
+  const int64_t nc = std::max<int64_t>(1, std::min<int64_t>({(int64_t)STREAM_MAXC, n, (total + STREAM_SPC - 1) / STREAM_SPC}));
+  int64_t acc = 0, c = 1, first = 0, ints = 1;
+  auto emit = [&](int64_t end) {
+    out.push_back(make_int4((int)first, (int)end, o[base + first], o[base + end]));
+    first = end;
+    ints = 1;
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    const int len = o[base + i + 1] - o[base + i];
+    if (i > first && ints + 3 + len > STREAM_SIDX_H) emit(i);
+    ints += 3 + len;
+    acc += (int64_t)len * per_edge + 2;
+    if (acc * nc >= total * c) {
+      if (i + 1 < n) emit(i + 1);
+      while (acc * nc >= total * c) ++c;
+    }
+  }
+  emit(n);
+  count = (int64_t)out.size() - at;
+}
+
 // a compacted item set over a subset of a layer's nodes (unary-sum aliases)
 struct AliasSet {
   int64_t off_base = 0, e_base = 0, map_base = 0, xmap_base = 0;  // into aoff[] / aidx[] / omap[]
   int64_t i_base = 0, i_n = 0, h_base = 0, h_n = 0, slots = 0;
   int64_t pmap_base = -1, pxmap_base = -1;  // padded per-item maps (pmap[] / pxmap[])
+  int64_t n = 0;                            // nodes of the set
 };
 
 struct LayerDesc {
@@ -325,6 +426,10 @@ struct LayerDesc {
   bool fa_on, fsum_redo, mrow_on, ba_on, bmask;
   bool bsum8;  // log-sum backward with 8-edge stage batches (children with > 4 parents common)
   AliasSet fa, ba;
+  // streaming kernel partitions (into d_scta; n = 0: set not eligible, a
+  // segment longer than one numpy pairwise block): forward plain / alias
+  // set, backward plain / alias set
+  int64_t fs_b = 0, fs_n = 0, fsa_b = 0, fsa_n = 0, bs_b = 0, bs_n = 0, bsa_b = 0, bsa_n = 0;
 };
 
 struct DeviceGuard {
@@ -386,6 +491,7 @@ struct KlayPlan {
   // (0 = none); no node of layers <= max head + 1 is aliased
   int32_t head_f = 0, head_b = 0, head_b_real = 0;
   int* d_microb = nullptr;
+  int4* d_scta = nullptr;  // streaming kernel CTAs (LayerDesc fs_b ...; build_stream_ctas)
 };
 
 extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
@@ -415,6 +521,7 @@ static void plan_free(KlayPlan* p) {
   cudaFree(p->d_pmap2);
   cudaFree(p->d_micro);
   cudaFree(p->d_microb);
+  cudaFree(p->d_scta);
   delete p;
 }
 
@@ -557,6 +664,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       d.fa.xmap_base = any_mrow ? (int64_t)omap.size() : -1;
       if (any_mrow) omap.insert(omap.end(), mr.begin(), mr.end());
       d.mrow_on = any_mrow;
+      d.fa.n = nc;
       build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0, !d.prod);
       add_set(fa, d.fa, aoff, (size_t)d.fa.off_base, aidx, (size_t)d.fa.e_base);
       p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
@@ -589,6 +697,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
         xs.push_back(logsum ? srow[l][c] : (int)(p->layer_row[l] + c));
         ++nc;
       }
+      d.ba.n = nc;
       d.ba.map_base = (int64_t)omap.size();
       omap.insert(omap.end(), outs.begin(), outs.end());
       d.ba.xmap_base = (int64_t)omap.size();
@@ -885,6 +994,15 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
                       const std::vector<int>& iv, size_t ib) { add_set(set, as, ov, ob, iv, ib); });
   }
   p->n_alias = (int64_t)alias_rows.size();
+  // streaming kernel partitions of every layer's node sets
+  std::vector<int4> scta;
+  for (int32_t l = 0; l < num_layers; ++l) {
+    LayerDesc& d = p->layers[l];
+    build_stream_ctas(off, (size_t)d.off_base, d.W, 1, scta, d.fs_b, d.fs_n);
+    if (d.fa_on) build_stream_ctas(aoff, (size_t)d.fa.off_base, d.fa.n, 1, scta, d.fsa_b, d.fsa_n);
+    build_stream_ctas(toff, (size_t)d.toff_base, d.Wprev, 2, scta, d.bs_b, d.bs_n);
+    if (d.ba_on) build_stream_ctas(aoff, (size_t)d.ba.off_base, d.ba.n, 2, scta, d.bsa_b, d.bsa_n);
+  }
 
   // roots (engine.py:203-212, 330-334)
   std::vector<int> rn(num_roots);
@@ -915,7 +1033,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       (rc = upload(&p->d_omap, omap)) || (rc = upload(&p->d_alias, alias_rows)) ||
       (rc = upload(&p->d_pidx, pidx)) || (rc = upload(&p->d_poff, poff)) ||
       (rc = upload(&p->d_pmap, pmap)) || (rc = upload(&p->d_pmap2, pxmap)) ||
-      (rc = upload(&p->d_micro, micro)) || (rc = upload(&p->d_microb, microb))) {
+      (rc = upload(&p->d_micro, micro)) || (rc = upload(&p->d_microb, microb)) ||
+      (rc = upload(&p->d_scta, scta))) {
     plan_free(p);
     return rc;
   }
@@ -1141,8 +1260,24 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     } else if (launch_on(d.prod ? KLAY_CLASS_FWD_PROD : KLAY_CLASS_FWD_SUM)) {
       a.hcount = hcount;
       LaunchScope ls(s, 0, l + 1);
-      if constexpr (U1) g_launches += launch_forward_layer_u1(d.prod, a, s);
-      else g_launches += launch_forward_layer(sr, d.prod, redo, a, s);
+      const bool aset = alias && d.fa_on;
+      const int64_t sb = aset ? d.fsa_b : d.fs_b, sn = aset ? d.fsa_n : d.fs_n;
+      if constexpr (U1) {
+        g_launches += launch_forward_layer_u1(d.prod, a, s);
+      } else if (sn > 0 && !g_no_stream) {
+        a.scta = reinterpret_cast<const int*>(p->d_scta + sb);
+        a.n_scta = (int)sn;
+#ifdef KLAY_STREAM_TRACE
+        const bool trace = g_trace_layer == l + 1 && g_trace_dir == 0;
+        if (trace) a.trace = stream_trace_buf();
+#endif
+        g_launches += launch_forward_stream(sr, d.prod, redo, a, s);
+#ifdef KLAY_STREAM_TRACE
+        if (trace) stream_trace_dump(a.trace, (int)sn * (int)((V + 255) / 256), l + 1, 0);
+#endif
+      } else {
+        g_launches += launch_forward_layer(sr, d.prod, redo, a, s);
+      }
     }
     prev = cur;
   }
@@ -1326,7 +1461,22 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
                       : (mode == BW_REALPROD_ ? KLAY_CLASS_BWD_REALPROD : KLAY_CLASS_BWD_LOGSUM);
       if (launch_on(cls)) {
         LaunchScope ls(s, 1, l + 1);
-        g_launches += launch_backward_layer(mode, a, s);
+        const bool aset = alias && d.ba_on;
+        const int64_t sb = aset ? d.bsa_b : d.bs_b, sn = aset ? d.bsa_n : d.bs_n;
+        if (sn > 0 && !g_no_stream) {
+          a.scta = reinterpret_cast<const int*>(p->d_scta + sb);
+          a.n_scta = (int)sn;
+#ifdef KLAY_STREAM_TRACE
+          const bool trace = g_trace_layer == l + 1 && g_trace_dir == 1;
+          if (trace) a.trace = stream_trace_buf();
+#endif
+          g_launches += launch_backward_stream(mode, a, s);
+#ifdef KLAY_STREAM_TRACE
+          if (trace) stream_trace_dump(a.trace, (int)sn * (int)((V + 255) / 256), l + 1, 1);
+#endif
+        } else {
+          g_launches += launch_backward_layer(mode, a, s);
+        }
       }
     }
   }

@@ -51,6 +51,12 @@ struct LayerArgs {
   const int* pmap;
   const int* pxmap;
   int rev;            // visit the column chunks last to first (L2 reuse across launches)
+  // streaming path (stream_kernels.cuh): node ranges of the CTAs (n_scta + 1
+  // entries over this set's nodes); spv / sring are set at launch
+  const int* scta;
+  int n_scta;
+  int spv, sring;
+  unsigned long long* trace;  // KLAY_STREAM_TRACE builds: per-CTA timing records (debug)
 };
 
 // The persistent tail kernel (thin upper layers in one launch) takes its
@@ -129,6 +135,12 @@ int launch_forward_layer(int sr, bool prod, bool alias, const LayerArgs<double>&
 // backward layer (BW_* mode): always a pairwise sum over each child's out-edges
 int launch_backward_layer(int mode, const LayerArgs<float>& a, cudaStream_t s);
 int launch_backward_layer(int mode, const LayerArgs<double>& a, cudaStream_t s);
+// the same layers on the bulk-copy streaming kernel (a.scta / a.n_scta set;
+// every segment of the set <= MICRO_FAN edges)
+int launch_forward_stream(int sr, bool prod, bool alias, const LayerArgs<float>& a, cudaStream_t s);
+int launch_forward_stream(int sr, bool prod, bool alias, const LayerArgs<double>& a, cudaStream_t s);
+int launch_backward_stream(int mode, const LayerArgs<float>& a, cudaStream_t s);
+int launch_backward_stream(int mode, const LayerArgs<double>& a, cudaStream_t s);
 
 // persistent tail: layers t.layer[0..n) in order, one cluster per column
 // chunk; returns the number of kernels launched (0 on a launch failure)

@@ -112,6 +112,7 @@ struct FwdGather {
   const T* base;
   long long ld;
   int nl;
+  __device__ __forceinline__ FwdGather() {}
   __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col, int nl_)
       : base(a.prev + col), ld(a.ld), nl(nl_) {}
   __device__ __forceinline__ const T* row_ptr(int row) const { return base + (long long)row * ld; }
@@ -160,6 +161,7 @@ struct BwdGather {
   long long ld;
   int nl;
   bool unary_ok;
+  __device__ __forceinline__ BwdGather() {}
   __device__ __forceinline__ BwdGather(const LayerArgs<T>& a, size_t col, int nl_)
       : gbase(a.gcur + col), nbase(a.ncur + col),
         // PASSA: the masks sit at the column chunk's start of the child rows

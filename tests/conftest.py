@@ -89,6 +89,34 @@ def rel_close(got, exp, rtol, atol_frac=0.0):
             f"{(err / np.maximum(np.abs(exp[fin]), 1e-300)).max():.3e}")
 
 
+def fp32_close(got, ref64, ref32, rtol=1e-5):
+    """Elementwise fp32 gate against the reference's own fp32 error: with
+    ref64 the reference in fp64 and ref32 the reference run in fp32,
+    |got - ref64| <= max(rtol * |ref64|, 2 * |ref32 - ref64|) at every finite
+    ref64 entry (no scale-relative slack), identical -inf/+inf/NaN positions
+    elsewhere. So an fp32 result may be off by the north star's rel 1e-5 or
+    by twice what the reference's own fp32 evaluation is off, whichever is
+    larger -- small gradients are checked at their own size."""
+    got = np.asarray(got, dtype=np.float64)
+    ref64 = np.asarray(ref64, dtype=np.float64)
+    ref32 = np.asarray(ref32, dtype=np.float64)
+    assert got.shape == ref64.shape == ref32.shape, (got.shape, ref64.shape, ref32.shape)
+    fin = np.isfinite(ref64)
+    assert np.array_equal(np.isnan(got[~fin]), np.isnan(ref64[~fin])), "NaN positions differ"
+    nonnan = ~fin & ~np.isnan(ref64)
+    assert np.array_equal(got[nonnan], ref64[nonnan]), "inf mismatch"
+    if fin.any():
+        with np.errstate(invalid="ignore"):
+            tol = np.maximum(rtol * np.abs(ref64[fin]), 2.0 * np.abs(ref32[fin] - ref64[fin]))
+        tol = np.where(np.isnan(tol), np.inf, tol)
+        err = np.abs(got[fin] - ref64[fin])
+        bad = ~(err <= tol)
+        assert not bad.any(), (
+            f"{bad.sum()} of {bad.size} beyond the fp32 gate; worst err/tol "
+            f"{np.max(err[bad] / np.maximum(tol[bad], 1e-300)):.3e} at ref {ref64[fin][bad][:3]}, "
+            f"got {got[fin][bad][:3]}, ref32 {ref32[fin][bad][:3]}")
+
+
 @pytest.fixture(scope="session")
 def cuda():
     import torch

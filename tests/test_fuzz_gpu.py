@@ -7,7 +7,7 @@ values). Real fp64: bit-exact; log fp64: rel 1e-12."""
 import numpy as np
 import pytest
 
-from conftest import rel_close
+from conftest import fp32_close, rel_close
 
 pytestmark = pytest.mark.gpu
 
@@ -85,7 +85,7 @@ def test_random_circuits_match_oracle(cuda, seed):
 def test_random_wide_circuits_all_semirings(cuda, seed):
     """Wider random circuits (regular layer kernels, aliases and routes at the
     default tail): fp32 real bit-exact vs the reference's own fp32 run, fp32 log
-    within rel 1e-5 of fp64, Boolean (bit-packed) and max-product bit-exact,
+    elementwise within max(1e-5 rel, 2x the reference's own fp32 error) of fp64, Boolean (bit-packed) and max-product bit-exact,
     seeded backward."""
     import torch
     from oracle import engine_port as oracle
@@ -114,8 +114,10 @@ def test_random_wide_circuits_all_semirings(cuda, seed):
     with np.errstate(all="ignore"):
         ref, tr = oracle.forward(tc, lw, "log")
         gref = oracle.backward(tc, tr, "log")
-    rel_close(out.cpu().numpy(), ref, 1e-5, 1e-5)
-    rel_close(g.cpu().numpy(), gref, 1e-5, 1e-5)
+        ref32, tr32 = oracle.forward(tc, lw.astype(np.float32), "log")  # the reference's own fp32 run
+        gref32 = oracle.backward(tc, tr32, "log")
+    fp32_close(out.cpu().numpy(), ref, ref32)
+    fp32_close(g.cpu().numpy(), gref, gref32)
     # Boolean on 0/1 inputs (bit-packed path) and max-product: bit-exact
     wb = (rng.uniform(size=w.shape) < 0.6).astype(np.float64)
     ref, _ = oracle.forward(tc, wb, "bool", retain=False)

@@ -1,11 +1,12 @@
 """Torch surface (CircuitModule / KlayFunction) and the config E training
 step: autograd gradients equal the reference backward with seed =
-grad_output (fp64 rel 1e-12; fp32 rel 1e-5 vs fp64)."""
+grad_output (fp64 rel 1e-12; fp32 elementwise vs fp64 within max(1e-5 rel,
+2x the reference's own fp32 error), conftest.fp32_close)."""
 
 import numpy as np
 import pytest
 
-from conftest import load_case, load_config, rel_close
+from conftest import fp32_close, load_case, load_config, rel_close
 
 pytestmark = pytest.mark.gpu
 
@@ -23,8 +24,15 @@ def test_module_forward_backward_matches_oracle(cuda):
             roots = layer(w)
             seed = torch.tensor(gold["seed"], dtype=dt, device=cuda)
             (roots * seed).sum().backward()
-            rel_close(roots.detach().cpu().numpy(), gold["log_out"], rtol)
-            rel_close(w.grad.cpu().numpy(), gold["log_grad_seed"], rtol, rtol)
+            if dt == torch.float64:
+                rel_close(roots.detach().cpu().numpy(), gold["log_out"], rtol)
+                rel_close(w.grad.cpu().numpy(), gold["log_grad_seed"], rtol, rtol)
+            else:  # elementwise vs the reference's own fp32 run (oracle, bit-identical)
+                with np.errstate(all="ignore"):
+                    o32, t32 = oracle.forward(tc, lw.astype(np.float32), "log")
+                    g32 = oracle.backward(tc, t32, "log", gold["seed"].astype(np.float32))
+                fp32_close(roots.detach().cpu().numpy(), gold["log_out"], o32)
+                fp32_close(w.grad.cpu().numpy(), gold["log_grad_seed"], g32)
         layer = CircuitModule(tc, "real")
         w = torch.tensor(gold["w_real"], dtype=torch.float64, device=cuda, requires_grad=True)
         layer(w).sum().backward()

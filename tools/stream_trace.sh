@@ -1,0 +1,6 @@
+# per-CTA timing of single streaming launches (debug build, see klay.cu stream_trace_dump)
+export KLAY_LIB=$PWD/paper_2410_11415_b200/libklay_trace.so
+for spec in "9 0" "10 0" "9 1" "10 1"; do
+  set -- $spec
+  KLAY_STREAM_TRACE_LAYER=$1 KLAY_STREAM_TRACE_DIR=$2 python tools/ncu_target.py 2 2>&1 | grep "stream trace"
+done
