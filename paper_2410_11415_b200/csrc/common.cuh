@@ -40,6 +40,53 @@ constexpr int PW_BLOCK = KLAY_PW_BLOCK;  // numpy pairwise block (128; other val
 // covers NV * 512 bytes of the row (per-edge bookkeeping amortized NV-fold).
 constexpr int NV = KLAY_NV;
 
+// ---- KLAY_CHECKS builds: run-time bounds checks of every global row access --
+// (compute-sanitizer is unavailable on the GPU pool; this is the stand-in).
+// A kernel copies the call's valid byte ranges (the values / trace buffer and
+// the workspace) into shared memory at entry (chk_enter); every ldv / stv /
+// cp.async below verifies its 16-byte access against them, records the first
+// violation in the call's record (klay.cu reads it after the call) and
+// redirects the access to the start of the values buffer instead of faulting.
+struct ChkRanges {
+  const char* lo[2];
+  const char* hi[2];
+  int* rec;  // [0] violations, [1] site, [2] kernel tag, [3] low bits of the address
+  int tag;
+};
+#ifdef KLAY_CHECKS
+static __shared__ ChkRanges klay_chk;
+__device__ __forceinline__ void chk_enter(const ChkRanges& c) {
+  if ((threadIdx.x & 31) == 0 && threadIdx.x < 32) klay_chk = c;
+  __syncthreads();
+}
+static __device__ __noinline__ const void* chk_fail(const void* p, int site) {
+  if (klay_chk.rec && atomicAdd(klay_chk.rec, 1) == 0) {
+    klay_chk.rec[1] = site;
+    klay_chk.rec[2] = klay_chk.tag;
+    klay_chk.rec[3] = (int)(reinterpret_cast<uintptr_t>(p) & 0x7fffffff);
+  }
+  return klay_chk.lo[0];
+}
+__device__ __forceinline__ const void* chk(const void* p, int site, int bytes) {
+  const char* c = static_cast<const char*>(p);
+  if (!klay_chk.rec) return p;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    if (c >= klay_chk.lo[i] && c + bytes <= klay_chk.hi[i]) return p;
+  return chk_fail(p, site);
+}
+template <typename T>
+__device__ __forceinline__ T* chkp(T* p, int site) {
+  return (T*)chk(p, site, (int)sizeof(T));
+}
+#define KLAY_CHK(p, site) chkp((p), (site))
+#define KLAY_CHK_N(p, site, n) ((decltype(p))chk((p), (site), (n)))
+#else
+__device__ __forceinline__ void chk_enter(const ChkRanges&) {}
+#define KLAY_CHK(p, site) (p)
+#define KLAY_CHK_N(p, site, n) (p)
+#endif
+
 template <typename T>
 struct alignas(16) Vec {
   static constexpr int N = NV * 16 / sizeof(T);
@@ -56,7 +103,7 @@ __device__ __forceinline__ Vec<float> ldv(const float* p, int nl) {
   Vec<float> r;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    const float4 u = __ldcg(reinterpret_cast<const float4*>(p + (q < nl ? q : nl - 1) * PSTRIDE<float>));
+    const float4 u = __ldcg(KLAY_CHK(reinterpret_cast<const float4*>(p + (q < nl ? q : nl - 1) * PSTRIDE<float>), 1));
     r.v[4 * q] = u.x; r.v[4 * q + 1] = u.y; r.v[4 * q + 2] = u.z; r.v[4 * q + 3] = u.w;
   }
   return r;
@@ -65,7 +112,7 @@ __device__ __forceinline__ Vec<double> ldv(const double* p, int nl) {
   Vec<double> r;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    const double2 u = __ldcg(reinterpret_cast<const double2*>(p + (q < nl ? q : nl - 1) * PSTRIDE<double>));
+    const double2 u = __ldcg(KLAY_CHK(reinterpret_cast<const double2*>(p + (q < nl ? q : nl - 1) * PSTRIDE<double>), 1));
     r.v[2 * q] = u.x; r.v[2 * q + 1] = u.y;
   }
   return r;
@@ -75,7 +122,7 @@ __device__ __forceinline__ Vec<unsigned> ldv(const unsigned* p, int nl) {
   Vec<unsigned> r;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    const uint4 u = __ldcg(reinterpret_cast<const uint4*>(p + (q < nl ? q : nl - 1) * PSTRIDE<unsigned>));
+    const uint4 u = __ldcg(KLAY_CHK(reinterpret_cast<const uint4*>(p + (q < nl ? q : nl - 1) * PSTRIDE<unsigned>), 1));
     r.v[4 * q] = u.x; r.v[4 * q + 1] = u.y; r.v[4 * q + 2] = u.z; r.v[4 * q + 3] = u.w;
   }
   return r;
@@ -84,7 +131,7 @@ __device__ __forceinline__ void stv(unsigned* p, const Vec<unsigned>& r, int na)
 #pragma unroll
   for (int q = 0; q < NV; ++q)
     if (q < na)
-      *reinterpret_cast<uint4*>(p + q * PSTRIDE<unsigned>) =
+      *KLAY_CHK(reinterpret_cast<uint4*>(p + q * PSTRIDE<unsigned>), 2) =
           make_uint4(r.v[4 * q], r.v[4 * q + 1], r.v[4 * q + 2], r.v[4 * q + 3]);
 }
 
@@ -93,13 +140,13 @@ __device__ __forceinline__ void stv(float* p, const Vec<float>& r, int na) {
 #pragma unroll
   for (int q = 0; q < NV; ++q)
     if (q < na)
-      *reinterpret_cast<float4*>(p + q * PSTRIDE<float>) =
+      *KLAY_CHK(reinterpret_cast<float4*>(p + q * PSTRIDE<float>), 2) =
           make_float4(r.v[4 * q], r.v[4 * q + 1], r.v[4 * q + 2], r.v[4 * q + 3]);
 }
 __device__ __forceinline__ void stv(double* p, const Vec<double>& r, int na) {
 #pragma unroll
   for (int q = 0; q < NV; ++q)
-    if (q < na) *reinterpret_cast<double2*>(p + q * PSTRIDE<double>) = make_double2(r.v[2 * q], r.v[2 * q + 1]);
+    if (q < na) *KLAY_CHK(reinterpret_cast<double2*>(p + q * PSTRIDE<double>), 2) = make_double2(r.v[2 * q], r.v[2 * q + 1]);
 }
 
 template <typename T>
@@ -305,9 +352,14 @@ struct LseOp {
 };
 
 // ---- cp.async (LDGSTS) helpers: 16-byte global -> shared copies ------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+// plan data (indices, offsets: not in the checked value ranges)
+__device__ __forceinline__ void cp_async16_plan(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// value rows (checked in KLAY_CHECKS builds)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  cp_async16_plan(smem, KLAY_CHK_N(gmem, 3, 16));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>

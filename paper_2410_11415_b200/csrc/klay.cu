@@ -249,6 +249,37 @@ struct LaunchScope {
   }
 };
 
+// KLAY_CHECKS builds: the call's valid ranges and a device violation record
+// (common.cuh chk); a call fails with KLAY_ECUDA when a kernel recorded one
+#ifdef KLAY_CHECKS
+int* chk_record() {
+  static int* rec = nullptr;
+  if (!rec) {
+    cudaMalloc(&rec, 4 * sizeof(int));
+    cudaMemset(rec, 0, 4 * sizeof(int));
+  }
+  return rec;
+}
+// KLAY_CHECKS_SHRINK=<bytes>: declare only that many bytes of the values /
+// trace buffer valid (negative control of the checker: legal accesses past
+// it must be reported, and are redirected instead of performed)
+ChkRanges chk_ranges(const void* buf, size_t buf_bytes, const void* work, size_t work_bytes) {
+  static const long long shrink = [] {
+    const char* e = getenv("KLAY_CHECKS_SHRINK");
+    return (e && *e) ? atoll(e) : -1LL;
+  }();
+  if (shrink >= 0 && (size_t)shrink < buf_bytes) buf_bytes = (size_t)shrink;
+  ChkRanges c{};
+  c.lo[0] = static_cast<const char*>(buf);
+  c.hi[0] = c.lo[0] + buf_bytes;
+  c.lo[1] = static_cast<const char*>(work);
+  c.hi[1] = work ? c.lo[1] + work_bytes : c.lo[1];
+  c.rec = chk_record();
+  return c;
+}
+int chk_finish(cudaStream_t s, const char* what);
+#endif
+
 struct ItemSet {
   std::vector<int4> items;
   std::vector<unsigned> masks;  // parallel to items
@@ -494,7 +525,32 @@ struct KlayPlan {
   int4* d_scta = nullptr;  // streaming kernel CTAs (LayerDesc fs_b ...; build_stream_ctas)
 };
 
-extern "C" const char* klay_version(void) { return "libklay 0.2 sm_100a"; }
+#ifdef KLAY_CHECKS
+namespace {
+int chk_finish(cudaStream_t s, const char* what) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return KLAY_OK;  // (graph capture: checked when run eagerly)
+  int h[4] = {0, 0, 0, 0};
+  KLAY_CUDA(cudaStreamSynchronize(s));
+  KLAY_CUDA(cudaMemcpy(h, chk_record(), sizeof h, cudaMemcpyDeviceToHost));
+  if (h[0] == 0) return KLAY_OK;
+  KLAY_CUDA(cudaMemset(chk_record(), 0, sizeof h));
+  char msg[200];
+  snprintf(msg, sizeof msg, "%s: bounds check failed: %d out-of-range accesses, first at site %d in layer %d (address low bits 0x%x)",
+           what, h[0], h[1], h[2], h[3]);
+  return fail(KLAY_ECUDA, msg);
+}
+}  // namespace
+#endif
+
+extern "C" const char* klay_version(void) {
+#ifdef KLAY_CHECKS
+  return "libklay 0.2 sm_100a (bounds-checked build)";
+#else
+  return "libklay 0.2 sm_100a";
+#endif
+}
 
 extern "C" const char* klay_last_error(void) { return g_err.c_str(); }
 
@@ -1136,6 +1192,11 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   const bool retain = retain_mode != 0;
   const int V = (int)(ld * (int64_t)sizeof(T) / 16);
   T* pingpong[2] = {values, values + (size_t)p->max_width * ld};
+#ifdef KLAY_CHECKS
+  const ChkRanges chk = chk_ranges(values, (size_t)(retain ? p->total_rows : 2 * p->max_width) * ld * sizeof(T), work,
+                                   (size_t)2 * p->max_fslots * ld * sizeof(T) +
+                                       counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld));
+#endif
   constexpr bool U1 = std::is_same<T, unsigned>::value;
   if (p->K > 0 && launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 2, 0);
@@ -1168,6 +1229,10 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
   MicroArgs<T> micro{}, head{};
   const int32_t head_f = (g_no_tail || g_no_micro || g_no_head || !micro_fits(V)) ? 0 : p->head_f;
   auto run_micro = [&](MicroArgs<T>& m, int32_t first) -> int {
+#ifdef KLAY_CHECKS
+    m.chk = chk;
+    m.chk.tag = 1000 + first;
+#endif
     m.csr = p->d_micro;
     m.V = V;
     m.ld = ld;
@@ -1208,6 +1273,10 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
       continue;
     }
     LayerArgs<T> a = layer_args<T>(p, d, true, V, ld);
+#ifdef KLAY_CHECKS
+    a.chk = chk;
+    a.chk.tag = l + 1;
+#endif
     const bool redo = alias && d.fsum_redo;
     if (alias && d.fa_on) {
       // the layer's own set: non-aliased nodes over re-mapped operands
@@ -1329,7 +1398,11 @@ int forward_impl(const KlayPlan* p, int sr, const void* weights, int wdt, T* val
     ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());
+#ifdef KLAY_CHECKS
+  return chk_finish(s, "klay_forward");
+#else
   return KLAY_OK;
+#endif
 }
 
 template <typename T>
@@ -1340,6 +1413,11 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   // of layers further down than the next)
   T* gtrace = work;
   T* scratch = work + (size_t)p->total_rows * ld;
+#ifdef KLAY_CHECKS
+  const ChkRanges chk = chk_ranges(trace, (size_t)p->total_rows * ld * sizeof(T), work,
+                                   ((size_t)p->total_rows + p->max_bslots) * ld * sizeof(T) +
+                                       counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld));
+#endif
   int* hcount = reinterpret_cast<int*>(scratch + (size_t)p->max_bslots * ld);
   if (p->max_heavy > 0) {
     const size_t nb = counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld);
@@ -1370,6 +1448,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   for (int32_t l = p->L - 1; l >= 0; --l) {
     const LayerDesc& d = p->layers[l];
     LayerArgs<T> a = layer_args<T>(p, d, false, V, ld);
+#ifdef KLAY_CHECKS
+    a.chk = chk;
+    a.chk.tag = -(l + 1);
+#endif
     a.out = gtrace + (size_t)d.prev_row * ld;
     a.gcur = gtrace + (size_t)d.row * ld;
     a.ncur = trace + (size_t)d.row * ld;
@@ -1399,6 +1481,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
       // weighted layers: log sums (softmax weights), real products (zero-safe)
       m.logsum[i] = (domain == SR_LOG_) ? (d.prod ? 0 : 1) : (d.prod ? 1 : 0);
       if (l == lowest && launch_on(KLAY_CLASS_BWD_MICRO)) {
+#ifdef KLAY_CHECKS
+        m.chk = chk;
+        m.chk.tag = -(1000 + l);
+#endif
         m.csr = p->d_microb;
         m.V = V;
         m.ld = ld;
@@ -1486,7 +1572,11 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());
+#ifdef KLAY_CHECKS
+  return chk_finish(s, "klay_backward");
+#else
   return KLAY_OK;
+#endif
 }
 
 int check_common(const KlayPlan* plan, int32_t dtype, int64_t batch, int64_t ld) {

@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace klay {
 
 template <typename T>
@@ -57,6 +59,7 @@ struct LayerArgs {
   int n_scta;
   int spv, sring;
   unsigned long long* trace;  // KLAY_STREAM_TRACE builds: per-CTA timing records (debug)
+  ChkRanges chk;              // KLAY_CHECKS builds: valid byte ranges + violation record
 };
 
 // The persistent tail kernel (thin upper layers in one launch) takes its
@@ -105,6 +108,7 @@ struct MicroArgs {
   int n, w_in, V;
   long long ld;
   T eps;
+  ChkRanges chk;
 };
 // backward micro tail: steps i = 0.. walk the micro layers top down; step i
 // computes the children's adjoints of one layer
@@ -122,6 +126,7 @@ struct MicroBwdArgs {
   const int* csr;
   int n, w_top, V, unary_ok;
   long long ld;
+  ChkRanges chk;
 };
 int launch_backward_micro(int domain, const MicroBwdArgs<float>& m, cudaStream_t s);
 int launch_backward_micro(int domain, const MicroBwdArgs<double>& m, cudaStream_t s);

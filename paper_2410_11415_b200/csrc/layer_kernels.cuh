@@ -84,7 +84,7 @@ __device__ __forceinline__ void store_mask(T* chunk0, const Vec<T>& v, int lane)
   if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < (N + 3) / 4; ++q)
-      reinterpret_cast<uint4*>(chunk0)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      *KLAY_CHK(reinterpret_cast<uint4*>(chunk0) + q, 4) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
 }
 // a stand-in own value with the mask's finiteness: 0 (finite) or -inf
@@ -200,7 +200,7 @@ struct BwdGather {
       unsigned w[NV * 4];
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(xbase + (size_t)j * ld) + q);
+        const uint4 u = __ldcg(KLAY_CHK(reinterpret_cast<const uint4*>(xbase + (size_t)j * ld) + q, 5));
         w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
       }
       return mask_to_x<T>(w, (int)(threadIdx.x & 31));
@@ -672,7 +672,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
       const int h = (int)ib->mask;
       __threadfence();
       __syncwarp();
-      int* cnt = a.hcount + (size_t)h * ((a.V + 32 * NV - 1) / (32 * NV)) + chunk;
+      int* cnt = KLAY_CHK(a.hcount + (size_t)h * ((a.V + 32 * NV - 1) / (32 * NV)) + chunk, 6);
       int last = 0;
       if (lane == 0) last = atomicAdd(cnt, 1) == __ldg(&a.heavy[h].z) - 1;
       last = __shfl_sync(0xffffffffu, last, 0);
@@ -702,6 +702,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
 template <typename T, int RK, typename G>
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(LayerArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  chk_enter(a.chk);
   using S = ItemsSmem<T, G>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * WARPS_PER_BLOCK + warp;
@@ -826,6 +827,7 @@ constexpr int COMBINE_LEAVES = 64;  // leaf partials staged per combine warp
 template <typename T, int RK, typename G>
 __global__ void __launch_bounds__(32) combine_kernel(LayerArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  chk_enter(a.chk);
   const int h = blockIdx.x;
   if (h >= a.n_heavy) return;
   process_heavy<T, RK, G>(a, h, blockIdx.y, threadIdx.x, reinterpret_cast<uint4*>(smem),
@@ -923,6 +925,7 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
     tail_kernel(const __grid_constant__ TailArgs<T> t) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem[];
+  chk_enter(t.layer[0].chk);
   cg::cluster_group cluster = cg::this_cluster();
   const int csize = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -1106,7 +1109,12 @@ __device__ __forceinline__ Vec<T> micro_sum(int n, F&& v) {
 
 template <typename T, int RK>
 __device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, int P, const int* idx, int n, T eps) {
-  auto v = [&](int e) { return lds1<T>(rows + (size_t)idx[e] * P); };
+  auto v = [&](int e) {
+#ifdef KLAY_CHECKS
+    if ((unsigned)idx[e] >= (unsigned)MICRO_WF) chk_fail(rows, 7);
+#endif
+    return lds1<T>(rows + (size_t)idx[e] * P);
+  };
   if constexpr (RK == RK_SUM) {
     return micro_sum<T>(n, v);
   } else if constexpr (RK == RK_LSE) {
@@ -1129,13 +1137,14 @@ __device__ __forceinline__ Vec<T> micro_reduce(const uint4* rows, int P, const i
 
 // stage `n` ints of plan CSR (16-byte aligned) into shared memory; not waited
 __device__ __forceinline__ void micro_stage_csr(int* dst, const int* src, int n) {
-  for (int i = threadIdx.x; i < (n + 3) / 4; i += blockDim.x) cp_async16(dst + 4 * i, src + 4 * i);
+  for (int i = threadIdx.x; i < (n + 3) / 4; i += blockDim.x) cp_async16_plan(dst + 4 * i, src + 4 * i);
 }
 
 template <typename T, int RKP, int RKS>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_kernel(const __grid_constant__ MicroArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
+  chk_enter(m.chk);
   constexpr int P = MICRO_PF, NW = MICRO_THREADS / P, CSR = MICRO_CSRF;
   constexpr size_t SET = (size_t)MICRO_WF * P;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1204,6 +1213,7 @@ template <typename T, int DOM>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_bwd_kernel(const __grid_constant__ MicroBwdArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
+  chk_enter(m.chk);
   constexpr int P = MICRO_PB, NW = MICRO_THREADS / P, CSR = MICRO_CSRB;
   constexpr size_t SET = (size_t)MICRO_WB * P;
   extern __shared__ __align__(16) unsigned char smem[];

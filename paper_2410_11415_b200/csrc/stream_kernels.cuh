@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
   constexpr bool BWD = TR::BWD, XSLOT = TR::XSLOT;
   extern __shared__ __align__(128) unsigned char stream_smem[];
   unsigned char* smem = stream_smem;
+  chk_enter(a.chk);
   const int R = a.sring, NGR = R / SG;
   const int pvmax = a.spv;
   const int nt = (pvmax + VP - 1) / VP;  // consumer threads
@@ -216,6 +217,13 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
                      : "memory");
       }
       __syncwarp();
+#ifdef KLAY_CHECKS
+      if (lane < cnt) {  // the whole row chunk inside a valid range
+        src = KLAY_CHK_N(src, 8, 16);
+        if (KLAY_CHK_N(reinterpret_cast<const char*>(src) + rowb - 16, 8, 16) != reinterpret_cast<const char*>(src) + rowb - 16)
+          src = reinterpret_cast<const T*>(klay_chk.lo[0]);
+      }
+#endif
       if (lane < cnt) bulk_row(ring + (size_t)(grp * SG + lane) * pvmax, src, rowb, &full[grp]);
     }
 #ifdef KLAY_STREAM_TRACE
@@ -441,10 +449,12 @@ inline void launch_stream_vp(const LayerArgs<T>& a, cudaStream_t s) {
   const unsigned chunks = (unsigned)((a.V + a.spv - 1) / a.spv);
   const size_t smem = StreamSmem::bytes(a.sring, a.spv, XS);
   static std::atomic<unsigned> configured{0};
-  if (needs_config(configured)) {
-    cudaFuncSetAttribute(stream_kernel<T, RK, G, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static std::atomic<size_t> smem_set{0};  // (per process; the ring size is fixed per process)
+  if (needs_config(configured) || smem > smem_set.load()) {
+    cudaFuncSetAttribute(stream_kernel<T, RK, G, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(stream_kernel<T, RK, G, VP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
+    smem_set = std::max(smem_set.load(), smem);
   }
   const int nt = (a.spv + VP - 1) / VP;
   cudaLaunchConfig_t cfg = {};
