@@ -1062,10 +1062,26 @@ inline int launch_tail(const TailArgs<T>& t, int cluster, cudaStream_t s) {
 // sequential products / max / min, the streaming logsumexp of LseOp.
 
 constexpr int MICRO_THREADS = 512;
-constexpr int MICRO_PF = MICRO_P;
-constexpr int MICRO_PB = MICRO_P;
-constexpr size_t MICRO_SMEM_F = (size_t)2 * MICRO_WF * MICRO_PF * 16 + (size_t)2 * MICRO_CSRF * sizeof(int);
-constexpr size_t MICRO_SMEM_B = (size_t)4 * MICRO_WB * MICRO_PB * 16 + (size_t)2 * MICRO_CSRB * sizeof(int);
+// P: 16-byte pieces per CTA column chunk. Two (32 bytes) when the batch has
+// more than one wave of CTAs' worth of pieces; one for small batches, which
+// doubles the CTAs (and halves their work) where the tails are latency-bound
+template <int P>
+constexpr size_t micro_smem_f() { return (size_t)2 * MICRO_WF * P * 16 + (size_t)2 * MICRO_CSRF * sizeof(int); }
+template <int P>
+constexpr size_t micro_smem_b() { return (size_t)4 * MICRO_WB * P * 16 + (size_t)2 * MICRO_CSRB * sizeof(int); }
+inline int micro_p(int V) {
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static const int forced = [] {
+    const char* e = getenv("KLAY_MICRO_P");
+    return (e && *e) ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  return V <= sms ? 1 : MICRO_P;
+}
 
 template <typename T>
 __device__ __forceinline__ Vec<T> lds1(const uint4* p) {
@@ -1140,12 +1156,12 @@ __device__ __forceinline__ void micro_stage_csr(int* dst, const int* src, int n)
   for (int i = threadIdx.x; i < (n + 3) / 4; i += blockDim.x) cp_async16_plan(dst + 4 * i, src + 4 * i);
 }
 
-template <typename T, int RKP, int RKS>
+template <typename T, int RKP, int RKS, int P>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_kernel(const __grid_constant__ MicroArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
   chk_enter(m.chk);
-  constexpr int P = MICRO_PF, NW = MICRO_THREADS / P, CSR = MICRO_CSRF;
+  constexpr int NW = MICRO_THREADS / P, CSR = MICRO_CSRF;
   constexpr size_t SET = (size_t)MICRO_WF * P;
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* rows = reinterpret_cast<uint4*>(smem);
@@ -1188,16 +1204,16 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
   }
 }
 
-template <typename T, int RKP, int RKS>
-inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
-  auto kern = micro_kernel<T, RKP, RKS>;
-  constexpr size_t bytes = MICRO_SMEM_F;
+template <typename T, int RKP, int RKS, int P>
+inline int launch_micro_p(const MicroArgs<T>& m, cudaStream_t s) {
+  auto kern = micro_kernel<T, RKP, RKS, P>;
+  constexpr size_t bytes = micro_smem_f<P>();
   static std::atomic<unsigned> configured{0};
   if (needs_config(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((m.V + MICRO_PF - 1) / MICRO_PF), 1, 1);
+  cfg.gridDim = dim3((unsigned)((m.V + P - 1) / P), 1, 1);
   cfg.blockDim = dim3(MICRO_THREADS, 1, 1);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
@@ -1209,12 +1225,17 @@ inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, m) == cudaSuccess ? 1 : 0;
 }
 
-template <typename T, int DOM>
+template <typename T, int RKP, int RKS>
+inline int launch_micro(const MicroArgs<T>& m, cudaStream_t s) {
+  return micro_p(m.V) == 1 ? launch_micro_p<T, RKP, RKS, 1>(m, s) : launch_micro_p<T, RKP, RKS, MICRO_P>(m, s);
+}
+
+template <typename T, int DOM, int P>
 __global__ void __launch_bounds__(MICRO_THREADS, 1)
     micro_bwd_kernel(const __grid_constant__ MicroBwdArgs<T> m) {
   static_assert(NV == 1, "the micro tail assumes one 16-byte piece per lane");
   chk_enter(m.chk);
-  constexpr int P = MICRO_PB, NW = MICRO_THREADS / P, CSR = MICRO_CSRB;
+  constexpr int NW = MICRO_THREADS / P, CSR = MICRO_CSRB;
   constexpr size_t SET = (size_t)MICRO_WB * P;
   extern __shared__ __align__(16) unsigned char smem[];
   uint4* gset = reinterpret_cast<uint4*>(smem);              // [2] adjoint row sets
@@ -1313,16 +1334,16 @@ __global__ void __launch_bounds__(MICRO_THREADS, 1)
   }
 }
 
-template <typename T, int DOM>
-inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
-  auto kern = micro_bwd_kernel<T, DOM>;
-  constexpr size_t bytes = MICRO_SMEM_B;
+template <typename T, int DOM, int P>
+inline int launch_micro_bwd_p(const MicroBwdArgs<T>& m, cudaStream_t s) {
+  auto kern = micro_bwd_kernel<T, DOM, P>;
+  constexpr size_t bytes = micro_smem_b<P>();
   static std::atomic<unsigned> configured{0};
   if (needs_config(configured)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((m.V + MICRO_PB - 1) / MICRO_PB), 1, 1);
+  cfg.gridDim = dim3((unsigned)((m.V + P - 1) / P), 1, 1);
   cfg.blockDim = dim3(MICRO_THREADS, 1, 1);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
@@ -1332,6 +1353,11 @@ inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, m) == cudaSuccess ? 1 : 0;
+}
+
+template <typename T, int DOM>
+inline int launch_micro_bwd(const MicroBwdArgs<T>& m, cudaStream_t s) {
+  return micro_p(m.V) == 1 ? launch_micro_bwd_p<T, DOM, 1>(m, s) : launch_micro_bwd_p<T, DOM, MICRO_P>(m, s);
 }
 
 }  // namespace klay
