@@ -91,12 +91,14 @@ KLAY_API int64_t klay_plan_num_nodes(const KlayPlan* plan);
 KLAY_API int64_t klay_plan_max_width(const KlayPlan* plan);
 /* Row offset of layer l (0 = inputs) inside the trace buffer. */
 KLAY_API int64_t klay_plan_layer_offset(const KlayPlan* plan, int32_t layer);
-/* The plan's schedule (out[6]): out[0] first layer of the persistent
+/* The plan's schedule (out[8]): out[0] first layer of the persistent
  * (cluster) tail, out[1] / out[2] first layer of the forward / backward (log
  * semiring) micro tail (0-based gate layers; L = none), out[3] number of
  * aliased (never written) rows of a backward-only trace, out[4] / out[5]
- * layers in the forward / backward micro head (0 = none). Returns 0, or
- * EINVAL for a null argument. */
+ * layers in the forward / backward micro head (0 = none), out[6] rows of the
+ * backward's adjoint buffer (node layers with disjoint lifetimes share
+ * rows), out[7] rows of the trace. Returns 0, or EINVAL for a null
+ * argument. */
 KLAY_API int klay_plan_schedule(const KlayPlan* plan, int64_t* out);
 
 /* Smallest legal row stride (elements) for batch B and element type. */

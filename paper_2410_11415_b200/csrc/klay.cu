@@ -484,6 +484,11 @@ struct KlayPlan {
   int32_t L = 0;
   int32_t R = 0;
   int64_t total_rows = 0;
+  // backward adjoint layout (klay_plan_create, assign_adjoint_blocks): node
+  // layer m's adjoint rows are rows [gbase[m], gbase[m] + W_m) of a buffer
+  // of adj_rows rows; layers whose lifetimes do not overlap share rows
+  std::vector<int64_t> gbase;
+  int64_t adj_rows = 0;
   int64_t max_width = 0;
   int64_t max_fslots = 0, max_bslots = 0;
   int64_t max_heavy = 0;  // heavy segments of the largest layer (leaf counters)
@@ -764,6 +769,55 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
     }
+  }
+}
+
+// Adjoint rows are needed only from their first write to their last read in
+// the backward sweep (time t = L-1-l while gate layer l runs): node layer m
+// is written by gate layer m (t = L-1-m; the seed writes layer L at t = -1)
+// or earlier by a route top above it (alias item sets: outs of gate layer l
+// landing in layer m at t = L-1-l), and read by gate layer m-1 (t = L-m) --
+// the micro tail reads layer L when it launches, a micro head its top layer
+// at t = L-1, and the gradient copy reads layer 0 at the end (t = L). Every
+// column chunk runs the layers in this order (grid dependencies between
+// layer kernels, barriers inside the tail / micro kernels), so layers with
+// disjoint lifetimes can share rows: blocks are placed first-fit in order of
+// first write. Config C (B = 1024 fp32): 4.16 GB of adjoints -> see
+// DESIGN.md §3.
+static void assign_adjoint_blocks(KlayPlan* p, const std::vector<int64_t>& first_write) {
+  const int L = p->L;
+  auto width = [&](int m) -> int64_t { return p->layer_row[m + 1 <= L ? m + 1 : L] - p->layer_row[m]; };
+  std::vector<int64_t> st(L + 1), en(L + 1);
+  for (int m = 0; m <= L; ++m) {
+    st[m] = std::min<int64_t>(m == L ? -1 : L - 1 - m, first_write[m]);
+    en[m] = (m == 0) ? L : L - m;
+  }
+  const int32_t mb = std::min(p->microb_from, p->microb_from_real);
+  en[L] = std::max<int64_t>(en[L], (int64_t)L - 1 - mb);
+  if (p->head_b > 0) en[p->head_b] = std::max<int64_t>(en[p->head_b], L - 1);
+  if (p->head_b_real > 0) en[p->head_b_real] = std::max<int64_t>(en[p->head_b_real], L - 1);
+  std::vector<int> order(L + 1);
+  for (int m = 0; m <= L; ++m) order[m] = m;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return st[a] < st[b]; });
+  struct Blk {
+    int64_t off, size, end;
+  };
+  std::vector<Blk> live;  // sorted by offset
+  p->gbase.assign(L + 1, 0);
+  p->adj_rows = 0;
+  for (int m : order) {
+    // blocks whose last read precedes this layer's first write are free
+    live.erase(std::remove_if(live.begin(), live.end(), [&](const Blk& b) { return b.end < st[m]; }), live.end());
+    std::sort(live.begin(), live.end(), [](const Blk& a, const Blk& b) { return a.off < b.off; });
+    const int64_t w = (m == L) ? p->WL : width(m);
+    int64_t at = 0;
+    for (const Blk& b : live) {
+      if (b.off - at >= w) break;
+      at = std::max(at, b.off + b.size);
+    }
+    p->gbase[m] = at;
+    live.push_back({at, w, en[m]});
+    p->adj_rows = std::max(p->adj_rows, at + w);
   }
 }
 
@@ -1050,6 +1104,35 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
                       const std::vector<int>& iv, size_t ib) { add_set(set, as, ov, ob, iv, ib); });
   }
   p->n_alias = (int64_t)alias_rows.size();
+  // backward adjoint blocks; alias item sets' absolute output rows (route
+  // bottoms, own rows) become adjoint-buffer rows
+  {
+    auto layer_of = [&](int64_t r) -> int {
+      return (int)(std::upper_bound(p->layer_row.begin(), p->layer_row.end(), r) - p->layer_row.begin()) - 1;
+    };
+    std::vector<int64_t> first_write(num_layers + 1, INT64_MAX);
+    for (int32_t l = 0; l < num_layers; ++l) {
+      const LayerDesc& d = p->layers[l];
+      if (!d.ba_on) continue;
+      for (int64_t j = 0; j < d.ba.n; ++j) {
+        const int m = layer_of(omap[(size_t)d.ba.map_base + j] & 0x7fffffff);
+        first_write[m] = std::min<int64_t>(first_write[m], (int64_t)num_layers - 1 - l);
+      }
+    }
+    assign_adjoint_blocks(p, first_write);
+    auto to_adj = [&](int v) -> int {
+      const int64_t r = v & 0x7fffffff;
+      const int m = layer_of(r);
+      return (int)(p->gbase[m] + (r - p->layer_row[m])) | (v & INT32_MIN);
+    };
+    for (int32_t l = 0; l < num_layers; ++l) {
+      const LayerDesc& d = p->layers[l];
+      if (!d.ba_on) continue;
+      for (int64_t j = 0; j < d.ba.n; ++j) omap[(size_t)d.ba.map_base + j] = to_adj(omap[(size_t)d.ba.map_base + j]);
+      // (the padded per-item copies: unused padding entries stay in range)
+      for (int64_t j = 0; j < d.ba.i_n * PADW_H; ++j) pmap[(size_t)d.ba.pmap_base + j] = to_adj(pmap[(size_t)d.ba.pmap_base + j]);
+    }
+  }
   // streaming kernel partitions of every layer's node sets
   std::vector<int4> scta;
   for (int32_t l = 0; l < num_layers; ++l) {
@@ -1116,6 +1199,8 @@ extern "C" int klay_plan_schedule(const KlayPlan* p, int64_t* out) {
   out[3] = p->n_alias;
   out[4] = p->head_f;
   out[5] = p->head_b;
+  out[6] = p->adj_rows;
+  out[7] = p->total_rows;
   return KLAY_OK;
 }
 extern "C" int64_t klay_plan_layer_offset(const KlayPlan* p, int32_t l) {
@@ -1146,7 +1231,7 @@ extern "C" size_t klay_forward_workspace(const KlayPlan* plan, int32_t dtype, in
 
 extern "C" size_t klay_backward_workspace(const KlayPlan* plan, int32_t dtype, int64_t ld) {
   if (!plan) return 0;
-  return ((size_t)plan->total_rows + plan->max_bslots) * ld * esize(dtype) +
+  return ((size_t)plan->adj_rows + plan->max_bslots) * ld * esize(dtype) +
          counter_bytes(plan, dtype, ld);
 }
 
@@ -1412,10 +1497,10 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   // adjoints: one row per node, laid out like the trace (routes write rows
   // of layers further down than the next)
   T* gtrace = work;
-  T* scratch = work + (size_t)p->total_rows * ld;
+  T* scratch = work + (size_t)p->adj_rows * ld;
 #ifdef KLAY_CHECKS
   const ChkRanges chk = chk_ranges(trace, (size_t)p->total_rows * ld * sizeof(T), work,
-                                   ((size_t)p->total_rows + p->max_bslots) * ld * sizeof(T) +
+                                   ((size_t)p->adj_rows + p->max_bslots) * ld * sizeof(T) +
                                        counter_bytes(p, sizeof(T) == 8 ? KLAY_F64 : KLAY_F32, ld));
 #endif
   int* hcount = reinterpret_cast<int*>(scratch + (size_t)p->max_bslots * ld);
@@ -1425,7 +1510,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   }
   if (launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 3, p->L + 1);
-    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, gtrace + (size_t)p->layer_row[p->L] * ld,
+    launch_seed<T>(seed, p->d_top_off, p->d_top_pos, gtrace + (size_t)p->gbase[p->L] * ld,
                    (int)p->WL, p->R, B, ld, s);
     ++g_launches;
   }
@@ -1452,8 +1537,8 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
     a.chk = chk;
     a.chk.tag = -(l + 1);
 #endif
-    a.out = gtrace + (size_t)d.prev_row * ld;
-    a.gcur = gtrace + (size_t)d.row * ld;
+    a.out = gtrace + (size_t)p->gbase[l] * ld;
+    a.gcur = gtrace + (size_t)p->gbase[l + 1] * ld;
     a.ncur = trace + (size_t)d.row * ld;
     a.nprev = trace + (size_t)d.prev_row * ld;
     a.scratch = scratch;
@@ -1568,7 +1653,7 @@ int backward_impl(const KlayPlan* p, int domain, const T* trace, int64_t ld, con
   }
   if (p->K > 0 && launch_on(KLAY_CLASS_BOUNDARY)) {
     LaunchScope ls(s, 3, 0);
-    launch_store_rows<T>(gtrace, grads, (int)p->K, B, ld, s);
+    launch_store_rows<T>(gtrace + (size_t)p->gbase[0] * ld, grads, (int)p->K, B, ld, s);
     ++g_launches;
   }
   KLAY_CUDA(cudaGetLastError());

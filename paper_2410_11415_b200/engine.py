@@ -229,13 +229,15 @@ class DevicePlan:
         self.max_width = int(lib.klay_plan_max_width(handle))
         self.layer_offsets = [int(lib.klay_plan_layer_offset(handle, l))
                               for l in range(self.num_layers + 1)]
-        sched = (ctypes.c_int64 * 6)()
+        sched = (ctypes.c_int64 * 8)()
         _lib.check(lib.klay_plan_schedule(handle, sched), "klay_plan_schedule")
         # {tail, micro, micro_bwd}: first 0-based gate layer of each tail
         # (num_layers = none); aliased rows of a backward-only trace; layers
-        # in the forward / backward micro heads
+        # in the forward / backward micro heads; rows of the backward's
+        # adjoint buffer (layers with disjoint lifetimes share rows)
         self.schedule = {"tail": sched[0], "micro": sched[1], "micro_bwd": sched[2],
-                         "aliased_rows": sched[3], "head": sched[4], "head_bwd": sched[5]}
+                         "aliased_rows": sched[3], "head": sched[4], "head_bwd": sched[5],
+                         "adjoint_rows": sched[6]}
 
     def __del__(self):
         h = getattr(self, "_handle", None)

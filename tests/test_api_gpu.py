@@ -7,7 +7,7 @@ import threading
 import numpy as np
 import pytest
 
-from conftest import load_case, rel_close
+from conftest import load_case, load_config, rel_close
 
 pytestmark = pytest.mark.gpu
 
@@ -123,3 +123,21 @@ def test_evaluate_semiring_accepts_semiring_objects(cuda):
         engine.evaluate_semiring(tc, w, ForeignSemiring("tropical", float("inf"), 0.0))
     with pytest.raises(engine.EvalError, match="identities"):
         engine.evaluate_semiring(tc, w, ForeignSemiring("real", 1.0, 0.0))
+
+
+def test_backward_workspace_shares_rows_between_layers(cuda):
+    """Adjoint rows of node layers with disjoint lifetimes share memory
+    (klay.cu assign_adjoint_blocks). Config C' (no unary chains: every
+    adjoint block lives two steps) needs 5 % of the trace's rows; config C's
+    adjoint routes keep layers live for up to ~10 steps, which bounds any
+    layer-granular layout at 0.786 of the trace: the plan
+    gets within 5 % of that bound."""
+    from paper_2410_11415_b200 import engine
+    for name, bound in (("Cp", 0.06), ("C", 0.786 * 1.05)):
+        tc, _ = load_config(name)
+        plan = engine.device_plan(tc, cuda)
+        rows = plan.schedule["adjoint_rows"]
+        assert rows <= bound * plan.num_nodes, (name, rows / plan.num_nodes)
+        ld = plan.row_stride(1024, np.float32)
+        work = int(plan._lib.klay_backward_workspace(plan.handle, 0, ld))
+        assert work < plan.num_nodes * ld * 4
