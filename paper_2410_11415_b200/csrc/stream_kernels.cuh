@@ -247,47 +247,36 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
     in_row[q] = pc < pv;
     pl[q] = min(pc, pv - 1);
   }
-  // Slots are consumed in order. A consumer waits for a group only when it
-  // has used up the groups it waited for, and first releases those (so a
-  // node longer than the ring cannot deadlock); every node end also releases
-  // the groups it finished, which lets the producer refill early.
-  int taken = 0;      // slots consumed
-  int ready = 0;      // slots of the groups waited for
-  int gw = 0, pw = 0;  // next group to wait for, its parity
-  int released = 0;   // groups released
-  const uint4* cur = ring;  // slot `taken` in the ring
-  const uint4* ring_end = ring + (size_t)R * pvmax;
-  auto release_done = [&]() {
-    // groups whose every slot is consumed (all of the CTA's at the end)
-    const int upto = (taken >= ns) ? (ns + SG - 1) / SG : taken / SG;
-    if (released < upto) {
-      __syncwarp();
-      if (lane == 0)
-        for (int gi = released; gi < upto; ++gi) mbar_arrive(&empty[gi % NGR]);
-      released = upto;
-    }
-  };
+  // Slots are consumed in order: wait for a group at its first slot,
+  // release it (empty barrier, one arrive per consumer warp) right after its
+  // last, so a node longer than the ring never deadlocks and the producer
+  // refills as early as possible. Running slot pointer, no divisions.
+  int gs = 0, grp = 0, par = 0;
+  const uint4* cur = ring;
   auto take = [&](Vec<T> (&v)[VP]) {
-    if (taken == ready) {
-      release_done();
-      KLAY_TWAIT(mbar_wait(&full[gw], pw));
-      ready += SG;
-      if (++gw == NGR) {
-        gw = 0;
-        pw ^= 1;
-      }
-    }
+    if (gs == 0) KLAY_TWAIT(mbar_wait(&full[grp], par));
 #pragma unroll
     for (int q = 0; q < VP; ++q) v[q] = lds1<T>(cur + pl[q]);
     cur += pvmax;
-    if (cur == ring_end) cur = ring;
-    ++taken;
+    if (++gs == SG) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[grp]);
+      gs = 0;
+      if (++grp == NGR) {
+        grp = 0;
+        par ^= 1;
+        cur = ring;
+      }
+    }
   };
   G gq[VP];
 #pragma unroll
   for (int q = 0; q < VP; ++q) gq[q] = G(a, col0 + (size_t)pl[q] * PIECE<T>, 1);
+  int eb = 0;  // (soff[0] == 0: offsets are relative to the CTA's first edge)
   for (int k = 0; k < nn; ++k) {
-    const int ea = soff[k], n = soff[k + 1] - ea;
+    const int ea = eb;
+    eb = soff[k + 1];
+    const int n = eb - ea;
     const int out = out_id(k);
     Vec<T> x[VP];
     if constexpr (XSLOT) {
@@ -299,7 +288,7 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
     int e = ea;
     // the next edge's contribution (its slots are next in the ring)
     auto next = [&](Vec<T> (&v)[VP]) {
-      const int row = (G::ROWV || XSLOT || BWD) ? sidx[e] : 0;
+      const int row = G::ROWV ? sidx[e] : 0;  // (alias sign, unary-parent flag, product zero path)
       ++e;
       take(v);
       if constexpr (BWD) {
@@ -400,7 +389,6 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
         for (int q = 0; q < VP; ++q) seq_combine<T, RK>(res[q], v[q]);
       }
     }
-    release_done();
 #pragma unroll
     for (int q = 0; q < VP; ++q) {
       const size_t col = col0 + (size_t)pl[q] * PIECE<T>;
@@ -420,8 +408,10 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
       }
     }
   }
-  taken = ns;
-  release_done();
+  if (gs != 0) {  // the last, partial group
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[grp]);
+  }
 #ifdef KLAY_STREAM_TRACE
   if (tr && tid == 0) {
     tr[5] = w_cyc;
