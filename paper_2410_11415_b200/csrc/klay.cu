@@ -43,7 +43,15 @@ constexpr int TASK_EDGES_BWD = KLAY_TASK_EDGES_BWD;  // backward short tasks
 constexpr int TASK_NODES_BWD = KLAY_TASK_NODES_BWD;
 constexpr int SHORT_FWD = 8;       // FwdGather::SE
 constexpr int PADW_H = 32;         // padded per-item index data (klay::PADW)
-constexpr int SHORT_BWD = 8;       // BwdGather::SE
+constexpr int SHORT_BWD = 8;       // segments of backward short tasks (numpy's sequential range)
+#ifndef KLAY_FWD_SE
+#define KLAY_FWD_SE 8
+#endif
+#ifndef KLAY_BWD_SE
+#define KLAY_BWD_SE 8
+#endif
+constexpr int BATCH_FWD = KLAY_FWD_SE;  // FwdGather::SE: edges per stage batch
+constexpr int BATCH_BWD = KLAY_BWD_SE;  // BwdGather<PASS / PASSA / REALPROD>::SE
 #ifndef KLAY_LOGSUM_SE
 #define KLAY_LOGSUM_SE 4
 #endif
@@ -318,7 +326,10 @@ const int LSE_LEAF_MIN = [] {  // (KLAY_LSE_LEAF: tuning experiments)
 }();
 void build_items(const std::vector<int>& off, size_t base, int W, int short_max, ItemSet& s,
                  bool split = true, int cap = 0, bool lse = false, int task_edges = TASK_EDGES_H,
-                 int task_nodes = TASK_NODES_H) {
+                 int task_nodes = TASK_NODES_H, int batch_max = 0) {
+  // stage batches of <= batch_max edges (default: short_max); short_max
+  // bounds the segments of short tasks
+  if (batch_max <= 0) batch_max = short_max;
   const int E = off[base + W] - off[base];
   if (cap <= 0) cap = std::max(short_max, std::min(task_edges, (E / 296) & ~7));
   std::vector<int4> leaves, longs, shorts;
@@ -333,7 +344,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
       int n0 = tb;
       while (n0 < end_node) {
         mask |= 1u << (n0 - tb);
-        const int lim = off[base + n0] + short_max;
+        const int lim = off[base + n0] + batch_max;
         int n1 = n0 + 1;
         while (n1 < end_node && off[base + n1 + 1] <= lim) ++n1;
         n0 = n1;
@@ -726,7 +737,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       if (any_mrow) omap.insert(omap.end(), mr.begin(), mr.end());
       d.mrow_on = any_mrow;
       d.fa.n = nc;
-      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0, !d.prod);
+      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0, !d.prod, TASK_EDGES_H,
+                  TASK_NODES_H, BATCH_FWD);
       add_set(fa, d.fa, aoff, (size_t)d.fa.off_base, aidx, (size_t)d.fa.e_base);
       p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)fa.heavy.size());
@@ -764,7 +776,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
       build_items(aoff, (size_t)d.ba.off_base, (int)nc, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
-                  ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD);
+                  ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
       add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
@@ -954,7 +966,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
         ? std::max(8, std::min(TASK_EDGES_H, (int)((E + TAIL_CLUSTER * TAIL_WARPS_H - 1) /
                                                    (TAIL_CLUSTER * TAIL_WARPS_H) + 7) & ~7))
         : 0;
-    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap);
+    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap, false, TASK_EDGES_H, TASK_NODES_H,
+                BATCH_FWD);
     // log-sum backward: 4-edge stage batches unless children with more
     // parents are common (> 5 %), which would otherwise all become long items
     if (!d.prod && l < tail_from) {
@@ -963,7 +976,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       d.bsum8 = many * 20 > prev_w;
     }
     build_items(toff, (size_t)d.toff_base, (int)prev_w, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
-                bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD);
+                bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());
@@ -973,7 +986,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     d.fq_n = d.fi_n;
     if (d.prod && !fs.heavy.empty()) {
       ItemSet qs;
-      build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, qs, false, tcap);
+      build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, qs, false, tcap, false, TASK_EDGES_H, TASK_NODES_H,
+                  BATCH_FWD);
       d.fq_base = (int64_t)items.size();
       d.fq_n = (int64_t)qs.items.size();
       items.insert(items.end(), qs.items.begin(), qs.items.end());
@@ -988,7 +1002,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       int maxn = 0;
       for (int64_t i = 0; i < W; ++i) maxn = std::max(maxn, off[d.off_base + i + 1] - off[d.off_base + i]);
       if (maxn - 1 > LSE_SPLIT) {
-        build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, ls, true, 0, true);
+        build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, ls, true, 0, true, TASK_EDGES_H, TASK_NODES_H,
+                    BATCH_FWD);
         d.fl_base = (int64_t)items.size();
         d.fl_n = (int64_t)ls.items.size();
         items.insert(items.end(), ls.items.begin(), ls.items.end());

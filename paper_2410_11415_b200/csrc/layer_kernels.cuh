@@ -51,6 +51,14 @@ constexpr int CHUNKS_PER_WARP = KLAY_CHUNKS_PER_WARP;
 #ifndef KLAY_LOGSUM_SE
 #define KLAY_LOGSUM_SE 4
 #endif
+// edges per stage batch of the forward and of the pass-through / real-product
+// backward (segments in short tasks stay <= 8 edges: numpy's sequential range)
+#ifndef KLAY_FWD_SE
+#define KLAY_FWD_SE 8
+#endif
+#ifndef KLAY_BWD_SE
+#define KLAY_BWD_SE 8
+#endif
 #ifndef KLAY_LOGSUM_MINB
 #define KLAY_LOGSUM_MINB 18
 #endif
@@ -105,7 +113,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 // the trace), as the logsumexp of one element (the child, NaN for +inf)
 template <typename T, bool ALIAS = false>
 struct FwdGather {
-  static constexpr int NOP = 1, NX = 0, SE = 8, XPIECES = 0;
+  static constexpr int NOP = 1, NX = 0, SE = KLAY_FWD_SE, XPIECES = 0;
   static constexpr int CAP = KLAY_FWD_STAGED_IDX;  // staged edge indices per item
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
@@ -147,7 +155,7 @@ struct BwdGather {
   // edges per stage batch: log-sum layers stage three rows per edge and are
   // shared-memory bound, so they use 4 (their segments are short); layers
   // whose children often have more parents use the 8-edge variant LOGSUM8
-  static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : 8;
+  static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : (MODE == BW_LOGSUM8 ? 8 : KLAY_BWD_SE);
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
