@@ -973,7 +973,11 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     if (!d.prod && l < tail_from) {
       int64_t many = 0;
       for (int64_t j = 0; j < prev_w; ++j) many += gcnt[j] > SHORT_BWD_SUM;
-      d.bsum8 = many * 20 > prev_w;
+      static const int force8 = [] {  // KLAY_LOGSUM8=0/1: A/B override
+        const char* e = getenv("KLAY_LOGSUM8");
+        return (e && *e) ? atoi(e) : -1;
+      }();
+      d.bsum8 = force8 >= 0 ? force8 == 1 : many * 20 > prev_w;
     }
     build_items(toff, (size_t)d.toff_base, (int)prev_w, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
                 bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
