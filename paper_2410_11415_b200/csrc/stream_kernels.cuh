@@ -29,6 +29,14 @@ namespace klay {
 constexpr int SG = 4;             // ring slots per mbarrier group
 constexpr int STREAM_MAX_PV = 256;  // 16-byte pieces per CTA column chunk (4 KB)
 
+// consumer threads for a chunk of spv pieces, VP per thread: a multiple of
+// 32, so the pieces a warp holds for one q are one aligned 512-byte column
+// chunk (the route masks' unit: lane = piece within the chunk, as in the
+// items kernel). Pieces past the row are clamped and never stored.
+__host__ __device__ constexpr int stream_threads(int spv, int vp) {
+  return ((spv + vp - 1) / vp + 31) / 32 * 32;
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
@@ -97,7 +105,7 @@ __global__ void __launch_bounds__(STREAM_MAX_PV / VP + 32, 3) stream_kernel(cons
   chk_enter(a.chk);
   const int R = a.sring, NGR = R / SG;
   const int pvmax = a.spv;
-  const int nt = (pvmax + VP - 1) / VP;  // consumer threads
+  const int nt = stream_threads(pvmax, VP);  // consumer threads
   const int ncw = (nt + 31) >> 5;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
   unsigned long long* empty = full + NGR;
@@ -446,7 +454,7 @@ inline void launch_stream_vp(const LayerArgs<T>& a, cudaStream_t s) {
                          cudaSharedmemCarveoutMaxShared);
     smem_set = std::max(smem_set.load(), smem);
   }
-  const int nt = (a.spv + VP - 1) / VP;
+  const int nt = stream_threads(a.spv, VP);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.n_scta, chunks);
   cfg.blockDim = dim3((unsigned)(((nt + 31) / 32 + 1) * 32));

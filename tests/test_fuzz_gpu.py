@@ -81,6 +81,48 @@ def test_random_circuits_match_oracle(cuda, seed):
         rel_close(nv[l], tr[l], 1e-12, 1e-12)
 
 
+def sweep_case(seed):
+    """tools/fuzz_sweep.py's case for a seed: a random shape, then (circuit,
+    batch, weights in (0.05, 0.95) with 4 % zeros), or None when the shape
+    is too narrow to draw."""
+    rng = np.random.default_rng(seed)
+    K = int(rng.integers(4, 120)) * 2
+    L = int(rng.integers(2, 16))
+    try:
+        tc = random_circuit(seed, K=K, L=L, wmax=int(rng.integers(8, 3000)), grow=int(rng.integers(1, 4)))
+    except ValueError:
+        return None
+    B = int(rng.integers(1, 300))
+    w = rng.uniform(0.05, 0.95, size=(B, tc.num_inputs))
+    w[rng.uniform(size=w.shape) < 0.04] = 0.0
+    return tc, B, w
+
+
+@pytest.mark.parametrize("seed", [52093, 52235, 52249, 52294])
+def test_route_masks_odd_row_widths(cuda, seed):
+    """Adjoint routes read the finiteness masks the forward leaves per
+    512-byte column chunk. Row widths that are not a multiple of two chunks
+    (these sweep seeds: fp64 B = 172, 141, 274, 293) once broke the streaming
+    kernel's mask layout (stream_kernels.cuh stream_threads); test_stream_gpu
+    runs this under KLAY_STREAM=1 too. Log fp64, backward-only trace."""
+    import torch
+    from oracle import engine_port as oracle
+    from paper_2410_11415_b200 import _lib, device_plan
+    tc, B, w = sweep_case(seed)
+    plan = device_plan(tc)
+    with np.errstate(divide="ignore"):
+        lw = np.log(w)
+    x = torch.tensor(lw, dtype=torch.float64, device=cuda)
+    out, vals = plan.forward(x, _lib.KLAY_LOG, np.float64)
+    g = plan.backward(vals, B, _lib.KLAY_LOG, np.float64)
+    with np.errstate(all="ignore"):
+        ref, tr = oracle.forward(tc, lw, "log")
+        gref = oracle.backward(tc, tr, "log")
+    assert plan.schedule["aliased_rows"] > 0 and (B * 8 // 16) % 64
+    rel_close(out.cpu().numpy(), ref, 1e-12, 1e-12)
+    rel_close(g.cpu().numpy(), gref, 1e-12, 1e-12)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_wide_circuits_all_semirings(cuda, seed):
     """Wider random circuits (regular layer kernels, aliases and routes at the
