@@ -87,6 +87,21 @@ __device__ __forceinline__ void chk_enter(const ChkRanges&) {}
 #define KLAY_CHK_N(p, site, n) (p)
 #endif
 
+// Row r of a [rows, ld] buffer whose row stride is ldb = ld * sizeof(T)
+// bytes (< 2 GB): a 32 x 32 -> 64-bit IMAD.WIDE instead of a 64-bit multiply
+// and shift (half the address instructions of a staged edge). row_at takes a
+// signed row (alias offsets below the base), row_atu a non-negative one.
+template <typename T>
+__device__ __forceinline__ T* row_at(T* p, int r, int ldb) {
+  using C = typename std::conditional<std::is_const<T>::value, const char, char>::type;
+  return reinterpret_cast<T*>(reinterpret_cast<C*>(p) + (long long)r * ldb);
+}
+template <typename T>
+__device__ __forceinline__ T* row_atu(T* p, unsigned r, unsigned ldb) {
+  using C = typename std::conditional<std::is_const<T>::value, const char, char>::type;
+  return reinterpret_cast<T*>(reinterpret_cast<C*>(p) + (unsigned long long)r * ldb);
+}
+
 template <typename T>
 struct alignas(16) Vec {
   static constexpr int N = NV * 16 / sizeof(T);

@@ -41,15 +41,18 @@ constexpr int TASK_NODES_H = KLAY_TASK_NODES;  // nodes per short task (<= TASK_
 #endif
 constexpr int TASK_EDGES_BWD = KLAY_TASK_EDGES_BWD;  // backward short tasks
 constexpr int TASK_NODES_BWD = KLAY_TASK_NODES_BWD;
-constexpr int SHORT_FWD = 8;       // FwdGather::SE
 constexpr int PADW_H = 32;         // padded per-item index data (klay::PADW)
-constexpr int SHORT_BWD = 8;       // segments of backward short tasks (numpy's sequential range)
 #ifndef KLAY_FWD_SE
 #define KLAY_FWD_SE 8
 #endif
 #ifndef KLAY_BWD_SE
 #define KLAY_BWD_SE 8
 #endif
+// segments of short tasks: numpy's sequential range (<= 8 edges), and never
+// more than a stage batch holds
+constexpr int SHORT_FWD = KLAY_FWD_SE < 8 ? KLAY_FWD_SE : 8;  // FwdGather::SE
+constexpr int SHORT_BWD = KLAY_BWD_SE < 8 ? KLAY_BWD_SE : 8;  // pass-through / real-product backward
+constexpr int SHORT_BWD8 = 8;                                  // BwdGather<LOGSUM8>::SE
 constexpr int BATCH_FWD = KLAY_FWD_SE;  // FwdGather::SE: edges per stage batch
 constexpr int BATCH_BWD = KLAY_BWD_SE;  // BwdGather<PASS / PASSA / REALPROD>::SE
 #ifndef KLAY_LOGSUM_SE
@@ -775,7 +778,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       omap.insert(omap.end(), outs.begin(), outs.end());
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
-      build_items(aoff, (size_t)d.ba.off_base, (int)nc, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
+      build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
                   ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
       add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
@@ -979,7 +982,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       }();
       d.bsum8 = force8 >= 0 ? force8 == 1 : many * 20 > prev_w;
     }
-    build_items(toff, (size_t)d.toff_base, (int)prev_w, (d.prod || d.bsum8) ? SHORT_BWD : SHORT_BWD_SUM,
+    build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
                 bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();

@@ -118,12 +118,12 @@ struct FwdGather {
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
   const T* base;
-  long long ld;
+  int ldb;  // row stride in bytes
   int nl;
   __device__ __forceinline__ FwdGather() {}
   __device__ __forceinline__ FwdGather(const LayerArgs<T>& a, size_t col, int nl_)
-      : base(a.prev + col), ld(a.ld), nl(nl_) {}
-  __device__ __forceinline__ const T* row_ptr(int row) const { return base + (long long)row * ld; }
+      : base(a.prev + col), ldb((int)(a.ld * (long long)sizeof(T))), nl(nl_) {}
+  __device__ __forceinline__ const T* row_ptr(int row) const { return row_at(base, row, ldb); }
   __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
     cp_async_vec(slot, lane, row_ptr(row), nl);
   }
@@ -166,7 +166,7 @@ struct BwdGather {
   const T* xbase;
   const int* foff;
   const int* fsrc;
-  long long ld;
+  unsigned ldb;  // row stride in bytes
   int nl;
   bool unary_ok;
   __device__ __forceinline__ BwdGather() {}
@@ -174,7 +174,8 @@ struct BwdGather {
       : gbase(a.gcur + col), nbase(a.ncur + col),
         // PASSA: the masks sit at the column chunk's start of the child rows
         xbase(a.nprev + (MODE == BW_PASSA ? col - (col % (32 * NV * PIECE<T>)) : col)),
-        foff(a.foff), fsrc(a.fsrc), ld(a.ld), nl(nl_), unary_ok(a.unary_ok != 0) {}
+        foff(a.foff), fsrc(a.fsrc), ldb((unsigned)(a.ld * (long long)sizeof(T))), nl(nl_),
+        unary_ok(a.unary_ok != 0) {}
   // Edge rows of the transposed CSR carry bit 31 when the parent is a unary
   // sum (klay.cu plan build); with epsilon 0 such a parent's value equals the
   // child's, so LOGSUM skips loading it (unary_ok) and every mode masks the bit.
@@ -182,19 +183,19 @@ struct BwdGather {
     return LOGSUMLIKE && unary_ok && row < 0;
   }
   __device__ __forceinline__ void issue(uint4* slot, int row, int lane) const {
-    const size_t r = (size_t)(row & 0x7fffffff);
-    cp_async_vec(slot, lane, gbase + r * ld, nl);
+    const unsigned r = (unsigned)row & 0x7fffffffu;
+    cp_async_vec(slot, lane, row_atu(gbase, r, ldb), nl);
     if constexpr (NOP == 2)
-      if (!unary_edge(row)) cp_async_vec(slot + NV * 32, lane, nbase + r * ld, nl);
+      if (!unary_edge(row)) cp_async_vec(slot + NV * 32, lane, row_atu(nbase, r, ldb), nl);
   }
   // own value of an output (omap entry `out`, value row `xrow`). PASSA:
   // flagged outputs only, as the finiteness mask at the chunk's start
   __device__ __forceinline__ void issue_x(uint4* slot, int out, int xrow, int lane) const {
     if (MODE == BW_PASSA) {
       if (out < 0 && lane < NV)
-        cp_async16(slot + lane, xbase + (size_t)xrow * ld + lane * (16 / sizeof(T)));
+        cp_async16(slot + lane, row_atu(xbase, (unsigned)xrow, ldb) + lane * (16 / sizeof(T)));
     } else {
-      cp_async_vec(slot, lane, xbase + (size_t)xrow * ld, nl);
+      cp_async_vec(slot, lane, row_atu(xbase, (unsigned)xrow, ldb), nl);
     }
   }
   __device__ __forceinline__ Vec<T> x_from_stage(const uint4* slot, int lane) const {
@@ -208,12 +209,12 @@ struct BwdGather {
       unsigned w[NV * 4];
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        const uint4 u = __ldcg(KLAY_CHK(reinterpret_cast<const uint4*>(xbase + (size_t)j * ld) + q, 5));
+        const uint4 u = __ldcg(KLAY_CHK(reinterpret_cast<const uint4*>(row_atu(xbase, (unsigned)j, ldb)) + q, 5));
         w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
       }
       return mask_to_x<T>(w, (int)(threadIdx.x & 31));
     }
-    return ldv(xbase + (size_t)xrow * ld, nl);
+    return ldv(row_atu(xbase, (unsigned)xrow, ldb), nl);
   }
   __device__ __forceinline__ Vec<T> value(const uint4* slot, int lane, int row, const Vec<T>& x) const {
     if constexpr (NOP == 2) {
@@ -224,11 +225,11 @@ struct BwdGather {
     }
   }
   __device__ __forceinline__ Vec<T> direct(int row, const Vec<T>& x) const {
-    const size_t r = (size_t)(row & 0x7fffffff);
-    const Vec<T> g = ldv(gbase + r * ld, nl);
+    const unsigned r = (unsigned)row & 0x7fffffffu;
+    const Vec<T> g = ldv(row_atu(gbase, r, ldb), nl);
     if constexpr (NOP == 2) {
       if (unary_edge(row)) return unary(g, x);
-      return combine(g, ldv(nbase + r * ld, nl), row, x);
+      return combine(g, ldv(row_atu(nbase, r, ldb), nl), row, x);
     } else {
       return g;
     }
@@ -288,7 +289,7 @@ struct BwdGather {
 #pragma unroll
     for (int c = 0; c < N; ++c) { pnz[c] = T(1); zc[c] = 0; }
     for (int s = s0; s < s1; ++s) {
-      const Vec<T> y = ldv(xbase + (size_t)__ldg(fsrc + s) * ld, nl);
+      const Vec<T> y = ldv(row_atu(xbase, (unsigned)__ldg(fsrc + s), ldb), nl);
 #pragma unroll
       for (int c = 0; c < N; ++c) {
         if (y.v[c] == T(0)) ++zc[c];
@@ -479,6 +480,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
   const int na = lc.na;
   const size_t col = lc.col;
   const long long ld = a.ld;
+  const unsigned ldbu = (unsigned)(ld * (long long)sizeof(T));  // row stride in bytes
   const int4 it = ib->it;
   const int ne = it.w - it.z;
   const G g(a, col, lc.nl);
@@ -577,10 +579,10 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
         if constexpr (G::MASKED_OUT) {
           if (id < 0) out = G::unary(out, x);
         }
-        stv(a.out + (size_t)(id & 0x7fffffff) * ld + col, out, na);
+        stv(row_atu(a.out + col, (unsigned)id & 0x7fffffffu, ldbu), out, na);
         if (a.mbase) {
           const int mr = wxmap[nd];
-          if (mr >= 0) store_mask(a.mbase + (size_t)mr * ld + col0, out, lane);
+          if (mr >= 0) store_mask(row_atu(a.mbase + col0, (unsigned)mr, ldbu), out, lane);
         }
       }
     }
@@ -703,7 +705,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
     if constexpr (G::MASKED_OUT) {
       if (node < 0) out = G::unary(out, x);
     }
-    stv(a.out + (size_t)(node & 0x7fffffff) * ld + col, out, na);
+    stv(row_atu(a.out + col, (unsigned)node & 0x7fffffffu, ldbu), out, na);
   }
 }
 
