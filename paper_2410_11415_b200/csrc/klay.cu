@@ -53,6 +53,10 @@ constexpr int PADW_H = 32;         // padded per-item index data (klay::PADW)
 constexpr int SHORT_FWD = KLAY_FWD_SE < 8 ? KLAY_FWD_SE : 8;  // FwdGather::SE
 constexpr int SHORT_BWD = KLAY_BWD_SE < 8 ? KLAY_BWD_SE : 8;  // pass-through / real-product backward
 constexpr int SHORT_BWD8 = 8;                                  // BwdGather<LOGSUM8>::SE
+#ifndef KLAY_LOGSUM8_XN
+#define KLAY_LOGSUM8_XN 2
+#endif
+constexpr int BATCH_NODES8 = KLAY_LOGSUM8_XN;  // BwdGather<LOGSUM8>::XN: nodes per stage batch
 constexpr int BATCH_FWD = KLAY_FWD_SE;  // FwdGather::SE: edges per stage batch
 constexpr int BATCH_BWD = KLAY_BWD_SE;  // BwdGather<PASS / PASSA / REALPROD>::SE
 #ifndef KLAY_LOGSUM_SE
@@ -329,9 +333,9 @@ const int LSE_LEAF_MIN = [] {  // (KLAY_LSE_LEAF: tuning experiments)
 }();
 void build_items(const std::vector<int>& off, size_t base, int W, int short_max, ItemSet& s,
                  bool split = true, int cap = 0, bool lse = false, int task_edges = TASK_EDGES_H,
-                 int task_nodes = TASK_NODES_H, int batch_max = 0) {
-  // stage batches of <= batch_max edges (default: short_max); short_max
-  // bounds the segments of short tasks
+                 int task_nodes = TASK_NODES_H, int batch_max = 0, int batch_nodes = 32) {
+  // stage batches of <= batch_max edges (default: short_max) and <=
+  // batch_nodes nodes; short_max bounds the segments of short tasks
   if (batch_max <= 0) batch_max = short_max;
   const int E = off[base + W] - off[base];
   if (cap <= 0) cap = std::max(short_max, std::min(task_edges, (E / 296) & ~7));
@@ -349,7 +353,7 @@ void build_items(const std::vector<int>& off, size_t base, int W, int short_max,
         mask |= 1u << (n0 - tb);
         const int lim = off[base + n0] + batch_max;
         int n1 = n0 + 1;
-        while (n1 < end_node && off[base + n1 + 1] <= lim) ++n1;
+        while (n1 < end_node && n1 - n0 < batch_nodes && off[base + n1 + 1] <= lim) ++n1;
         n0 = n1;
       }
       short_masks.push_back(mask);
@@ -779,7 +783,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
       build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
-                  ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
+                  ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0,
+                  (!d.prod && d.bsum8) ? BATCH_NODES8 : 32);
       add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
@@ -983,7 +988,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       d.bsum8 = force8 >= 0 ? force8 == 1 : many * 20 > prev_w;
     }
     build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
-                bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0);
+                bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0,
+                (!d.prod && d.bsum8) ? BATCH_NODES8 : 32);
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());

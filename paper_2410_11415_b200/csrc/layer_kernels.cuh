@@ -65,6 +65,14 @@ constexpr int CHUNKS_PER_WARP = KLAY_CHUNKS_PER_WARP;
 #ifndef KLAY_LOGSUM8_MINB
 #define KLAY_LOGSUM8_MINB 8
 #endif
+// own-value slots per stage batch of the 8-edge log-sum backward: batches
+// hold at most this many nodes (klay.cu build_items), so a stage reserves
+// own values for 2 nodes instead of 8 (children of these layers average
+// several parents). 11 instead of 8 resident warps per SM: config C'
+// log-sum backward 3.64 -> 2.91 ms (XN 4: 3.11, 3: 3.08, 1: 2.96)
+#ifndef KLAY_LOGSUM8_XN
+#define KLAY_LOGSUM8_XN 2
+#endif
 
 
 // ---- operand policies -------------------------------------------------------
@@ -113,7 +121,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 // the trace), as the logsumexp of one element (the child, NaN for +inf)
 template <typename T, bool ALIAS = false>
 struct FwdGather {
-  static constexpr int NOP = 1, NX = 0, SE = KLAY_FWD_SE, XPIECES = 0;
+  static constexpr int NOP = 1, NX = 0, SE = KLAY_FWD_SE, XPIECES = 0, XN = 0;
   static constexpr int CAP = KLAY_FWD_STAGED_IDX;  // staged edge indices per item
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
@@ -157,6 +165,7 @@ struct BwdGather {
   // whose children often have more parents use the 8-edge variant LOGSUM8
   static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : (MODE == BW_LOGSUM8 ? 8 : KLAY_BWD_SE);
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
+  static constexpr int XN = (MODE == BW_LOGSUM8) ? KLAY_LOGSUM8_XN : SE;  // own values per stage batch
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
                                  : (MODE == BW_PASSA ? KLAY_PASS_MINB
@@ -347,7 +356,7 @@ struct ItemsSmem {
   // stage units: 16-byte pieces; a staged vector is NV x 32 lanes of pieces
   static constexpr int EV = G::NOP * NV * 32;      // pieces per staged edge
   static constexpr int XV = G::NX * G::XPIECES;    // pieces per staged own value
-  static constexpr int STAGE_V = SE * (EV + XV);   // pieces per stage
+  static constexpr int STAGE_V = SE * EV + G::XN * XV;  // pieces per stage (<= XN nodes per batch)
   static constexpr size_t stage_bytes = (size_t)2 * STAGE_V * 16;
   // + one ItemIndex
 #ifndef KLAY_WARP_ALIGN
