@@ -63,6 +63,10 @@ constexpr int BATCH_BWD = KLAY_BWD_SE;  // BwdGather<PASS / PASSA / REALPROD>::S
 #define KLAY_LOGSUM_SE 4
 #endif
 constexpr int SHORT_BWD_SUM = KLAY_LOGSUM_SE;  // BwdGather<LOGSUM>::SE (sum layers)
+#ifndef KLAY_LOGSUM_XN
+#define KLAY_LOGSUM_XN KLAY_LOGSUM_SE
+#endif
+constexpr int BATCH_NODES4 = KLAY_LOGSUM_XN;   // BwdGather<LOGSUM>::XN
 #ifndef KLAY_PW_BLOCK
 #define KLAY_PW_BLOCK 128
 #endif
@@ -784,7 +788,7 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       omap.insert(omap.end(), xs.begin(), xs.end());
       build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
                   ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0,
-                  (!d.prod && d.bsum8) ? BATCH_NODES8 : 32);
+                  d.prod ? 32 : (d.bsum8 ? BATCH_NODES8 : BATCH_NODES4));
       add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)ba.heavy.size());
@@ -989,7 +993,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     }
     build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
                 bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0,
-                (!d.prod && d.bsum8) ? BATCH_NODES8 : 32);
+                d.prod ? 32 : (d.bsum8 ? BATCH_NODES8 : BATCH_NODES4));
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
     items.insert(items.end(), fs.items.begin(), fs.items.end());

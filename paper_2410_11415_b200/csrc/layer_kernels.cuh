@@ -73,6 +73,9 @@ constexpr int CHUNKS_PER_WARP = KLAY_CHUNKS_PER_WARP;
 #ifndef KLAY_LOGSUM8_XN
 #define KLAY_LOGSUM8_XN 2
 #endif
+#ifndef KLAY_LOGSUM_XN
+#define KLAY_LOGSUM_XN KLAY_LOGSUM_SE  // (the 4-edge log-sum backward: no cap)
+#endif
 
 
 // ---- operand policies -------------------------------------------------------
@@ -165,7 +168,8 @@ struct BwdGather {
   // whose children often have more parents use the 8-edge variant LOGSUM8
   static constexpr int SE = (MODE == BW_LOGSUM) ? KLAY_LOGSUM_SE : (MODE == BW_LOGSUM8 ? 8 : KLAY_BWD_SE);
   static constexpr int XPIECES = (MODE == BW_PASSA) ? NV : NV * 32;  // staged own value
-  static constexpr int XN = (MODE == BW_LOGSUM8) ? KLAY_LOGSUM8_XN : SE;  // own values per stage batch
+  static constexpr int XN = (MODE == BW_LOGSUM8) ? KLAY_LOGSUM8_XN
+                            : (MODE == BW_LOGSUM ? KLAY_LOGSUM_XN : SE);  // own values per stage batch
   static constexpr int MINB = (MODE == BW_PASS) ? KLAY_PASS_MINB
                               : (MODE == BW_LOGSUM ? KLAY_LOGSUM_MINB
                                  : (MODE == BW_PASSA ? KLAY_PASS_MINB
