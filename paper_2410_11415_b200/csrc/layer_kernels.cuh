@@ -125,6 +125,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = KLAY_FWD_SE, XPIECES = 0, XN = 0;
+  static constexpr bool FWD = true;
   static constexpr int CAP = KLAY_FWD_STAGED_IDX;  // staged edge indices per item
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
@@ -157,6 +158,7 @@ struct FwdGather {
 template <typename T, int MODE>
 struct BwdGather {
   static constexpr bool PASSLIKE = (MODE == BW_PASS || MODE == BW_PASSA);
+  static constexpr bool FWD = false;
   static constexpr bool LOGSUMLIKE = (MODE == BW_LOGSUM || MODE == BW_LOGSUM8);
   static constexpr int CAP = TASK_EDGES;  // staged edge indices per item
   static constexpr int NOP = PASSLIKE ? 1 : 2;
@@ -410,7 +412,12 @@ using ItemRegs = ItemRegsT<TASK_EDGES>;
 // Longer items load their indices after the descriptor.
 constexpr int PADW = 32;
 
-template <typename T, int CAP = TASK_EDGES>
+// The maps are normalized here, once per item, so the per-node code reads
+// them unconditionally: wmap = output row of item node `lane` (the node id
+// itself without an omap); wxmap = own-value row (backward; the node id
+// without an xmap) or, forward, the mask row (-1: no mask, also whenever the
+// call stores no masks).
+template <typename T, bool FWD, int CAP = TASK_EDGES>
 __device__ __forceinline__ ItemRegsT<CAP> item_regs_from(const LayerArgs<T>& a, int k, int4 it,
                                                          unsigned mask, int lane) {
   ItemRegsT<CAP> r;
@@ -419,8 +426,9 @@ __device__ __forceinline__ ItemRegsT<CAP> item_regs_from(const LayerArgs<T>& a, 
   const size_t pk = (size_t)k * PADW + lane;
   const int p0 = __ldg(a.pidx + pk);
   const int o0 = __ldg(a.poff + pk);
-  r.map = a.pmap ? __ldg(a.pmap + pk) : 0;
-  r.xmap = a.pxmap ? __ldg(a.pxmap + pk) : 0;
+  r.map = a.pmap ? __ldg(a.pmap + pk) : it.x + lane;
+  if (FWD) r.xmap = (a.pxmap && a.mbase) ? __ldg(a.pxmap + pk) : -1;
+  else r.xmap = a.pxmap ? __ldg(a.pxmap + pk) : it.x + lane;
   const int ne = r.it.w - r.it.z;
   if (ne <= PADW) {
     r.idx[0] = p0;
@@ -437,9 +445,9 @@ __device__ __forceinline__ ItemRegsT<CAP> item_regs_from(const LayerArgs<T>& a, 
   return r;
 }
 
-template <typename T, int CAP = TASK_EDGES>
+template <typename T, bool FWD, int CAP = TASK_EDGES>
 __device__ __forceinline__ ItemRegsT<CAP> load_item_regs(const LayerArgs<T>& a, int item, int lane) {
-  return item_regs_from<T, CAP>(a, item, __ldg(a.items + item), __ldg(a.masks + item), lane);
+  return item_regs_from<T, FWD, CAP>(a, item, __ldg(a.items + item), __ldg(a.masks + item), lane);
 }
 
 template <int CAP>
@@ -494,6 +502,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
   const size_t col = lc.col;
   const long long ld = a.ld;
   const unsigned ldbu = (unsigned)(ld * (long long)sizeof(T));  // row stride in bytes
+  T* const outc = a.out + col;  // this lane's column of the output rows
   const int4 it = ib->it;
   const int ne = it.w - it.z;
   const G g(a, col, lc.nl);
@@ -507,8 +516,8 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
     const int nb = it.x, nn = it.y - it.x;
     // node id of item node nd: output row / own-value row (omap: compacted
     // item sets and alias outputs, see LayerArgs)
-    auto nid = [&](int nd) { return a.omap ? wmap[nd] : nb + nd; };
-    auto xid = [&](int nd) { return a.xmap ? wxmap[nd] : nb + nd; };
+    auto nid = [&](int nd) { return wmap[nd]; };   // (maps normalized: item_regs_from)
+    auto xid = [&](int nd) { return wxmap[nd]; };
     const size_t col0 = (size_t)chunk * 32 * NV * PIECE<T>;  // the chunk's first column
     unsigned m_issue = ib->mask, m_scan = ib->mask;
     auto next_batch = [&](unsigned& m, int& n0, int& n1) {
@@ -592,8 +601,8 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
         if constexpr (G::MASKED_OUT) {
           if (id < 0) out = G::unary(out, x);
         }
-        stv(row_atu(a.out + col, (unsigned)id & 0x7fffffffu, ldbu), out, na);
-        if (a.mbase) {
+        stv(row_atu(outc, (unsigned)id & 0x7fffffffu, ldbu), out, na);
+        if constexpr (G::FWD) {
           const int mr = wxmap[nd];
           if (mr >= 0) store_mask(row_atu(a.mbase + col0, (unsigned)mr, ldbu), out, lane);
         }
@@ -604,8 +613,8 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
 
   // ===================== long segment / leaf =====================
   const bool leaf = it.y < 0;
-  const int node = a.omap ? wmap[0] : it.x;  // output (see the short path)
-  const int xnode = a.xmap ? wxmap[0] : it.x;
+  const int node = wmap[0];  // output (see the short path)
+  const int xnode = wxmap[0];
   const int t0 = leaf ? 0 : 1;      // first tail edge (relative)
   const int m = ne - t0;            // tail length
   Vec<T> x{};
@@ -711,14 +720,14 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
     if constexpr (RK == RK_SUM) out = (m == 0) ? x0 : vadd(x0, res);
     else if constexpr (RK == RK_LSE) out = lse.result();
     else out = acc;
-    if (a.mbase) {  // (all lanes: ballots)
+    if constexpr (G::FWD) {  // (all lanes: ballots)
       if (xnode >= 0) store_mask(a.mbase + (size_t)xnode * ld + (size_t)chunk * 32 * NV * PIECE<T>, out, lane);
     }
     if (na == 0) return;
     if constexpr (G::MASKED_OUT) {
       if (node < 0) out = G::unary(out, x);
     }
-    stv(row_atu(a.out + col, (unsigned)node & 0x7fffffffu, ldbu), out, na);
+    stv(row_atu(outc, (unsigned)node & 0x7fffffffu, ldbu), out, na);
   }
 }
 
@@ -735,7 +744,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, G::MINB) items_kernel(La
   // The item's index data is plan data: load it before waiting on the
   // previous layer's kernel (programmatic dependent launch, launch_layer),
   // and let the next layer's blocks start their own prologue meanwhile.
-  const ItemRegsT<G::CAP> r = load_item_regs<T, G::CAP>(a, item, lane);
+  const ItemRegsT<G::CAP> r = load_item_regs<T, G::FWD, G::CAP>(a, item, lane);
 #ifndef KLAY_NO_GDC
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -946,6 +955,7 @@ __device__ __forceinline__ void cluster_wait() {
 template <typename T, int RKP, int RKS, typename GP, typename GS>
 __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
     tail_kernel(const __grid_constant__ TailArgs<T> t) {
+  static_assert(GP::FWD == GS::FWD, "a tail runs one direction");
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem[];
   chk_enter(t.layer[0].chk);
@@ -993,7 +1003,7 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
   __syncwarp();
   ItemRegs next;
   if (t.n > 0 && w < t.layer[0].n_items)
-    next = item_regs_from(t.layer[0], w, desc[0].it, desc[0].mask, lane);
+    next = item_regs_from<T, GP::FWD>(t.layer[0], w, desc[0].it, desc[0].mask, lane);
   // all of the above is plan data: wait for the previous kernel's values
   // only now (programmatic dependent launch), and let the next kernel's
   // blocks take the SMs the tail leaves idle for their own prologue
@@ -1006,11 +1016,11 @@ __global__ void __launch_bounds__(TailSmem<T, GP, GS>::warps * 32, 1)
     stamp(i, 0);
     const ItemRegs cur = next;
     if (i + 1 < t.n && w < t.layer[i + 1].n_items)
-      next = item_regs_from(t.layer[i + 1], w, desc[i + 1].it, desc[i + 1].mask, lane);
+      next = item_regs_from<T, GP::FWD>(t.layer[i + 1], w, desc[i + 1].it, desc[i + 1].mask, lane);
     if (!t.debug_skip) {
       for (int it = w; it < a.n_items; it += cw) {
         __syncwarp();  // previous item done with ib
-        store_item_regs(ib, it == w ? cur : load_item_regs(a, it, lane), lane);
+        store_item_regs(ib, it == w ? cur : load_item_regs<T, GP::FWD>(a, it, lane), lane);
         __syncwarp();
         if (a.prod) run_item<T, RKP, GP>(a, ib, chunk, stage, lane);
         else run_item<T, RKS, GS>(a, ib, chunk, stage, lane);
