@@ -699,17 +699,24 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
     }
     if (a.hcount) {
       // the warp that writes the last leaf partial of (segment, chunk)
-      // finishes the segment in tree order (threadfence reduction: partials
-      // published before the count, read back through L2 after it)
+      // finishes the segment in tree order. The warp's partial stores are
+      // ordered before lane 0's counter increment by __syncwarp, and that
+      // increment is an acquire-release atomic at GPU scope: every partial
+      // published before its count is visible to the warp that takes the
+      // last count (read back through L2 after it). (One MEMBAR.ALL instead
+      // of two sequentially consistent __threadfence()s.)
       const int h = (int)ib->mask;
-      __threadfence();
       __syncwarp();
       int* cnt = KLAY_CHK(a.hcount + (size_t)h * ((a.V + 32 * NV - 1) / (32 * NV)) + chunk, 6);
       int last = 0;
-      if (lane == 0) last = atomicAdd(cnt, 1) == __ldg(&a.heavy[h].z) - 1;
+      if (lane == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+        last = (int)old == __ldg(&a.heavy[h].z) - 1;
+      }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        __threadfence();
+        __syncwarp();  // (orders the other lanes' reads after lane 0's acquire)
         // (inlined: an out-of-line call here costs the whole kernel ~10%)
         process_heavy<T, RK, G>(a, h, chunk, lane, stage, 2 * STAGE_V);
         if (lane == 0) *cnt = 0;  // ready for the next layer / pass
