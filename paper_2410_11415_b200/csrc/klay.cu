@@ -33,6 +33,17 @@ constexpr int TASK_EDGES_H = KLAY_TASK_EDGES;  // edges per short task (<= TASK_
 #define KLAY_TASK_NODES 16
 #endif
 constexpr int TASK_NODES_H = KLAY_TASK_NODES;  // nodes per short task (<= TASK_NODES)
+// forward sum (log-sum-exp) layers: smaller short tasks (more warps per
+// layer for their longer per-edge work): fwd_sum 0.289 -> 0.285 ms at B = 1024,
+// 0.122 -> 0.113 ms at B = 128 (config C); product layers keep 32 / 16
+#ifndef KLAY_TASK_EDGES_SUM
+#define KLAY_TASK_EDGES_SUM 24
+#endif
+#ifndef KLAY_TASK_NODES_SUM
+#define KLAY_TASK_NODES_SUM 12
+#endif
+constexpr int TASK_EDGES_S = KLAY_TASK_EDGES_SUM;
+constexpr int TASK_NODES_S = KLAY_TASK_NODES_SUM;
 #ifndef KLAY_TASK_EDGES_BWD
 #define KLAY_TASK_EDGES_BWD 48  // (32: -0.3 %, 64: -0.7 %)
 #endif
@@ -748,8 +759,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       if (any_mrow) omap.insert(omap.end(), mr.begin(), mr.end());
       d.mrow_on = any_mrow;
       d.fa.n = nc;
-      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0, !d.prod, TASK_EDGES_H,
-                  TASK_NODES_H, BATCH_FWD);
+      build_items(aoff, (size_t)d.fa.off_base, (int)nc, SHORT_FWD, fa, true, 0, !d.prod,
+                  d.prod ? TASK_EDGES_H : TASK_EDGES_S, d.prod ? TASK_NODES_H : TASK_NODES_S, BATCH_FWD);
       add_set(fa, d.fa, aoff, (size_t)d.fa.off_base, aidx, (size_t)d.fa.e_base);
       p->max_fslots = std::max<int64_t>(p->max_fslots, fa.slots);
       p->max_heavy = std::max<int64_t>(p->max_heavy, (int64_t)fa.heavy.size());
@@ -978,8 +989,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
         ? std::max(8, std::min(TASK_EDGES_H, (int)((E + TAIL_CLUSTER * TAIL_WARPS_H - 1) /
                                                    (TAIL_CLUSTER * TAIL_WARPS_H) + 7) & ~7))
         : 0;
-    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap, false, TASK_EDGES_H, TASK_NODES_H,
-                BATCH_FWD);
+    build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, fs, true, tcap, false,
+                d.prod ? TASK_EDGES_H : TASK_EDGES_S, d.prod ? TASK_NODES_H : TASK_NODES_S, BATCH_FWD);
     // log-sum backward: 4-edge stage batches unless children with more
     // parents are common (> 5 %), which would otherwise all become long items
     if (!d.prod && l < tail_from) {
@@ -1019,7 +1030,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       int maxn = 0;
       for (int64_t i = 0; i < W; ++i) maxn = std::max(maxn, off[d.off_base + i + 1] - off[d.off_base + i]);
       if (maxn - 1 > LSE_SPLIT) {
-        build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, ls, true, 0, true, TASK_EDGES_H, TASK_NODES_H,
+        build_items(off, (size_t)d.off_base, (int)W, SHORT_FWD, ls, true, 0, true, TASK_EDGES_S, TASK_NODES_S,
                     BATCH_FWD);
         d.fl_base = (int64_t)items.size();
         d.fl_n = (int64_t)ls.items.size();
