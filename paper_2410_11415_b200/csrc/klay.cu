@@ -52,6 +52,18 @@ constexpr int TASK_NODES_S = KLAY_TASK_NODES_SUM;
 #endif
 constexpr int TASK_EDGES_BWD = KLAY_TASK_EDGES_BWD;  // backward short tasks
 constexpr int TASK_NODES_BWD = KLAY_TASK_NODES_BWD;
+// children of sum layers with 4-edge stage batches (log-sum / real pass
+// backward): smaller tasks, bwd_logsum 0.524 -> 0.511 ms at B = 1024,
+// 0.149 -> 0.128 ms at B = 128, config E +6.6 % (8-edge LOGSUM8 layers keep
+// 48 / 24: C' -0.7 % otherwise)
+#ifndef KLAY_TASK_EDGES_BWD_SUM
+#define KLAY_TASK_EDGES_BWD_SUM 24
+#endif
+#ifndef KLAY_TASK_NODES_BWD_SUM
+#define KLAY_TASK_NODES_BWD_SUM 12
+#endif
+constexpr int TASK_EDGES_BWDS = KLAY_TASK_EDGES_BWD_SUM;
+constexpr int TASK_NODES_BWDS = KLAY_TASK_NODES_BWD_SUM;
 constexpr int PADW_H = 32;         // padded per-item index data (klay::PADW)
 #ifndef KLAY_FWD_SE
 #define KLAY_FWD_SE 8
@@ -798,7 +810,8 @@ static void build_aliases(KlayPlan* p, int64_t K, const int64_t* widths, const i
       d.ba.xmap_base = (int64_t)omap.size();
       omap.insert(omap.end(), xs.begin(), xs.end());
       build_items(aoff, (size_t)d.ba.off_base, (int)nc, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
-                  ba, true, 0, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0,
+                  ba, true, 0, false, (d.prod || d.bsum8) ? TASK_EDGES_BWD : TASK_EDGES_BWDS,
+                  (d.prod || d.bsum8) ? TASK_NODES_BWD : TASK_NODES_BWDS, d.prod ? BATCH_BWD : 0,
                   d.prod ? 32 : (d.bsum8 ? BATCH_NODES8 : BATCH_NODES4));
       add_set(ba, d.ba, aoff, (size_t)d.ba.off_base, aidx, (size_t)d.ba.e_base);
       p->max_bslots = std::max<int64_t>(p->max_bslots, ba.slots);
@@ -1003,7 +1016,8 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
       d.bsum8 = force8 >= 0 ? force8 == 1 : many * 20 > prev_w;
     }
     build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
-                bs, true, tcap, false, TASK_EDGES_BWD, TASK_NODES_BWD, d.prod ? BATCH_BWD : 0,
+                bs, true, tcap, false, (d.prod || d.bsum8) ? TASK_EDGES_BWD : TASK_EDGES_BWDS,
+                  (d.prod || d.bsum8) ? TASK_NODES_BWD : TASK_NODES_BWDS, d.prod ? BATCH_BWD : 0,
                 d.prod ? 32 : (d.bsum8 ? BATCH_NODES8 : BATCH_NODES4));
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
