@@ -125,7 +125,7 @@ __device__ __forceinline__ Vec<T> mask_to_x(const unsigned* w, int lane) {
 template <typename T, bool ALIAS = false>
 struct FwdGather {
   static constexpr int NOP = 1, NX = 0, SE = KLAY_FWD_SE, XPIECES = 0, XN = 0;
-  static constexpr bool FWD = true;
+  static constexpr bool FWD = true, MASKX = false;
   static constexpr int CAP = KLAY_FWD_STAGED_IDX;  // staged edge indices per item
   static constexpr bool ROWV = ALIAS, MASKED_OUT = false, ALIAS_IN = ALIAS;
   static constexpr int MINB = KLAY_FWD_MINB;  // resident blocks per SM (shared memory allows 25)
@@ -165,6 +165,9 @@ struct BwdGather {
   static constexpr int NX = (MODE == BW_PASS) ? 0 : 1;
   // (outputs flagged in omap carry the unary weight: own value or mask needed)
   static constexpr bool ROWV = (NOP == 2), MASKED_OUT = (NX == 1), ALIAS_IN = false;
+  // PASSA stages the own value only as a finiteness mask, used only by
+  // flagged outputs: read it there (mask_weight), not for every node
+  static constexpr bool MASKX = (MODE == BW_PASSA);
   // edges per stage batch: log-sum layers stage three rows per edge and are
   // shared-memory bound, so they use 4 (their segments are short); layers
   // whose children often have more parents use the 8-edge variant LOGSUM8
@@ -216,6 +219,15 @@ struct BwdGather {
   __device__ __forceinline__ Vec<T> x_from_stage(const uint4* slot, int lane) const {
     if (MODE == BW_PASSA) return mask_to_x<T>(reinterpret_cast<const unsigned*>(slot), lane);
     return lds_vec<T>(slot, lane);
+  }
+  // PASSA, flagged output: unary(g, x) straight from the staged mask bits
+  // (g where the child's value is finite, g * 0 elsewhere)
+  __device__ __forceinline__ static Vec<T> mask_weight(Vec<T> g, const uint4* slot, int lane) {
+    const unsigned* w = reinterpret_cast<const unsigned*>(slot);
+#pragma unroll
+    for (int c = 0; c < Vec<T>::N; ++c)
+      if (!((w[c] >> lane) & 1u)) g.v[c] = g.v[c] * T(0);
+    return g;
   }
   __device__ __forceinline__ Vec<T> load_x(int out, int xrow) const {
     if (MODE == BW_PASSA) {
@@ -551,7 +563,7 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
       for (int nd = n0; nd < n1; ++nd) {
         const int sb = woff[nd] - eb, n = woff[nd + 1] - woff[nd];
         Vec<T> x{};
-        if constexpr (G::NX) x = g.x_from_stage(st + SE * EV + (nd - n0) * XV, lane);
+        if constexpr (G::NX && !G::MASKX) x = g.x_from_stage(st + SE * EV + (nd - n0) * XV, lane);
         auto val = [&](int e) {
           return g.value(st + e * EV, lane, G::ROWV ? widx[eb + e] : 0, x);
         };
@@ -599,7 +611,10 @@ __device__ __forceinline__ void run_item(const LayerArgs<T>& a, const ItemIndexT
         }
         const int id = nid(nd);
         if constexpr (G::MASKED_OUT) {
-          if (id < 0) out = G::unary(out, x);
+          if (id < 0) {
+            if constexpr (G::MASKX) out = G::mask_weight(out, st + SE * EV + (nd - n0) * XV, lane);
+            else out = G::unary(out, x);
+          }
         }
         stv(row_atu(outc, (unsigned)id & 0x7fffffffu, ldbu), out, na);
         if constexpr (G::FWD) {
