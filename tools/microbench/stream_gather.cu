@@ -166,6 +166,63 @@ __global__ void staged(const float4* __restrict__ prev, float4* __restrict__ cur
   }
 }
 
+// The same per-warp staged pattern, but each batch's row chunks are moved by
+// lane-parallel bulk copies (lane i: edge i's 512-byte chunk) completing on
+// a per-stage mbarrier, instead of 32 lanes x 16-byte LDGSTS per edge.
+__global__ void staged_bulk(const float4* __restrict__ prev, float4* __restrict__ cur, const int* __restrict__ off,
+                            const int* __restrict__ src, const int2* __restrict__ tasks, int ntask, int V) {
+  extern __shared__ float4 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  float4* st = sm + warp * 2 * 8 * 32;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + nw * 2 * 8 * 32) + 2 * warp;
+  const int t = blockIdx.x * nw + warp;
+  if (t >= ntask) return;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+  const int2 tk = tasks[t];
+  const int v = blockIdx.y * 32 + lane;
+  int nb_[33], nbat = 0;
+  {
+    int n = tk.x;
+    while (n < tk.y) {
+      nb_[nbat++] = n;
+      const int lim = off[n] + 8;
+      int m = n + 1;
+      while (m < tk.y && off[m + 1] <= lim) ++m;
+      n = m;
+    }
+    nb_[nbat] = tk.y;
+  }
+  unsigned ph = 0;
+  auto issue = [&](int b) {
+    const int e0 = off[nb_[b]], e1 = off[nb_[b + 1]];
+    __syncwarp();  // every lane is done with this stage
+    if (lane == 0) mbar_expect(&bar[b & 1], (unsigned)(e1 - e0) * 512u);
+    __syncwarp();
+    if (lane < e1 - e0)
+      bulk_g2s(st + (b & 1) * 256 + lane * 32, prev + (size_t)src[e0 + lane] * V + blockIdx.y * 32, 512u, &bar[b & 1]);
+  };
+  issue(0);
+  for (int b = 0; b < nbat; ++b) {
+    if (b + 1 < nbat) issue(b + 1);
+    mbar_wait(&bar[b & 1], (ph >> (b & 1)) & 1u);
+    ph ^= 1u << (b & 1);
+    const int e0 = off[nb_[b]];
+    for (int n = nb_[b]; n < nb_[b + 1]; ++n) {
+      float4 acc = make_float4(0, 0, 0, 0);
+      for (int e = off[n]; e < off[n + 1]; ++e) {
+        float4 x = st[(b & 1) * 256 + (e - e0) * 32 + lane];
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      }
+      cur[(size_t)n * V + v] = acc;
+    }
+  }
+}
+
 int main(int argc, char** argv) {
   FILE* f = fopen(argc > 1 ? argv[1] : "layer.bin", "rb");
   if (!f) return 1;
@@ -224,6 +281,10 @@ int main(int argc, char** argv) {
     size_t smem = 2 * 8 * 32 * 16;
     timeit([&] { staged<<<grid, 32, smem>>>(prev, cur, doff, dsrc, dt, (int)tasks.size(), PV); },
            "staged (short segments only)");
+    CK(cudaFuncSetAttribute(staged_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 16));
+    timeit([&] { staged_bulk<<<grid, 32, smem + 16>>>(prev, cur, doff, dsrc, dt, (int)tasks.size(), PV); },
+           "staged, lane-parallel bulk copies");
+    if (argc > 2 && atoi(argv[2]) < 0) return 0;  // (staged variants only)
   }
   int sms = 148;
   const int only = argc > 2 ? atoi(argv[2]) : 0;
