@@ -1017,7 +1017,7 @@ extern "C" int klay_plan_create(int64_t num_inputs, int32_t num_layers, const in
     }
     build_items(toff, (size_t)d.toff_base, (int)prev_w, d.prod ? SHORT_BWD : (d.bsum8 ? SHORT_BWD8 : SHORT_BWD_SUM),
                 bs, true, tcap, false, (d.prod || d.bsum8) ? TASK_EDGES_BWD : TASK_EDGES_BWDS,
-                  (d.prod || d.bsum8) ? TASK_NODES_BWD : TASK_NODES_BWDS, d.prod ? BATCH_BWD : 0,
+                (d.prod || d.bsum8) ? TASK_NODES_BWD : TASK_NODES_BWDS, d.prod ? BATCH_BWD : 0,
                 d.prod ? 32 : (d.bsum8 ? BATCH_NODES8 : BATCH_NODES4));
     d.fi_base = (int64_t)items.size();
     d.fi_n = (int64_t)fs.items.size();
